@@ -1,0 +1,147 @@
+"""Python face of the CPU oracle (oracle.c) — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this package.  The product package
+paper_1304_5553_b200 never imports it (tests/test_isolation.py checks).
+
+Every function is a thin ctypes call into oracle.c, which cites the PAPER.md
+passage it follows.  Inputs are numpy arrays; results are numpy arrays or
+Python scalars.  Parity pins: tests/test_oracle.py.
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "liboracle.so")
+
+F32, F64, I32, I64 = 0, 1, 2, 3
+SUM, MAX, MIN = 0, 1, 2
+MAP_ID, MAP_MUL, MAP_SQUARE = 0, 1, 2
+INCLUSIVE, EXCLUSIVE = 0, 1
+
+_DT = {np.dtype(np.float32): F32, np.dtype(np.float64): F64,
+       np.dtype(np.int32): I32, np.dtype(np.int64): I64}
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-std=c11", "-fPIC", "-shared"]
+
+
+def build(force=False):
+    """Compile oracle.c with gcc (no FMA contraction, no fast-math)."""
+    src = os.path.join(HERE, "oracle.c")
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", *CFLAGS, "-o", LIB, src, "-lm"])
+    return LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(LIB)
+        vp, i64, i32, d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+        f32 = ctypes.c_float
+        for name, st in (("f32", f32), ("f64", d), ("i32", i32), ("i64", i64)):
+            fn = getattr(L, f"oracle_axpbyz_{name}")
+            fn.restype = None
+            fn.argtypes = [i64, st, vp, st, vp, vp]
+            fn = getattr(L, f"oracle_axpbz_{name}")
+            fn.restype = None
+            fn.argtypes = [i64, st, vp, st, vp]
+        L.oracle_sum_f32.restype = d
+        L.oracle_sum_f32.argtypes = [ctypes.c_int, i64, vp, vp, ctypes.POINTER(d)]
+        L.oracle_sum_f64.restype = d
+        L.oracle_sum_f64.argtypes = [ctypes.c_int, i64, vp, vp, ctypes.POINTER(d)]
+        L.oracle_sum_int.restype = i64
+        L.oracle_sum_int.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, i64, vp, vp]
+        L.oracle_maxmin_f32.restype = d
+        L.oracle_maxmin_f32.argtypes = [ctypes.c_int, ctypes.c_int, i64, vp, vp]
+        L.oracle_maxmin_f64.restype = d
+        L.oracle_maxmin_f64.argtypes = [ctypes.c_int, ctypes.c_int, i64, vp, vp]
+        L.oracle_maxmin_int.restype = i64
+        L.oracle_maxmin_int.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, i64, vp, vp]
+        L.oracle_scan_i32.restype = None
+        L.oracle_scan_i32.argtypes = [ctypes.c_int, i64, vp, vp, i32]
+        L.oracle_scan_i64.restype = None
+        L.oracle_scan_i64.argtypes = [ctypes.c_int, i64, vp, vp, i64]
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return a.ctypes.data if a is not None and a.size else None
+
+
+def _c(a, dt=None):
+    a = np.ascontiguousarray(a, dtype=dt)
+    return a
+
+
+def _name(dt):
+    return {F32: "f32", F64: "f64", I32: "i32", I64: "i64"}[_DT[np.dtype(dt)]]
+
+
+def axpbyz(a, x, b, y):
+    """z = a*x + b*y elementwise; a, b are cast to x.dtype (R2)."""
+    x = _c(x)
+    y = _c(y, x.dtype)
+    assert x.shape == y.shape and x.ndim == 1
+    z = np.empty_like(x)
+    st = x.dtype.type
+    getattr(lib(), f"oracle_axpbyz_{_name(x.dtype)}")(x.size, st(a).item(), _ptr(x), st(b).item(), _ptr(y), _ptr(z))
+    return z
+
+
+def axpbz(a, x, b):
+    """z = a*x + b elementwise (Listing 1/2 doubling is a=2, b=0)."""
+    x = _c(x)
+    z = np.empty_like(x)
+    st = x.dtype.type
+    getattr(lib(), f"oracle_axpbz_{_name(x.dtype)}")(x.size, st(a).item(), _ptr(x), st(b).item(), _ptr(z))
+    return z
+
+
+def reduce(op, map_, x, y=None, out_dtype=None, return_sumabs=False):
+    """Map-reduce.  Float SUM returns a float64 near-exact
+    value (Neumaier); integer SUM returns a Python int wrapped to out_dtype;
+    MAX/MIN returns a value of the input dtype."""
+    x = _c(x)
+    if map_ == MAP_MUL:
+        y = _c(y, x.dtype)
+        assert y.shape == x.shape
+    else:
+        y = None
+    in_dt = _DT[x.dtype]
+    out_dt = _DT[np.dtype(out_dtype)] if out_dtype is not None else in_dt
+    L = lib()
+    n = x.size
+    if op == SUM:
+        if in_dt in (F32, F64):
+            sa = ctypes.c_double(0.0)
+            fn = L.oracle_sum_f32 if in_dt == F32 else L.oracle_sum_f64
+            r = fn(map_, n, _ptr(x), _ptr(y), ctypes.byref(sa))
+            return (r, sa.value) if return_sumabs else r
+        r = int(L.oracle_sum_int(map_, in_dt, out_dt, n, _ptr(x), _ptr(y)))
+        return (r, None) if return_sumabs else r
+    if in_dt == F32:
+        r = np.float32(L.oracle_maxmin_f32(op, map_, n, _ptr(x), _ptr(y)))
+    elif in_dt == F64:
+        r = np.float64(L.oracle_maxmin_f64(op, map_, n, _ptr(x), _ptr(y)))
+    else:
+        r = int(L.oracle_maxmin_int(op, map_, in_dt, n, _ptr(x), _ptr(y)))
+    return (r, None) if return_sumabs else r
+
+
+def scan(kind, x, carry=0, out=None):
+    """Prefix sum; exclusive head = carry (neutral 0 by default)."""
+    x = _c(x)
+    if out is None:
+        out = np.empty_like(x)
+    fn = {np.dtype(np.int32): lib().oracle_scan_i32, np.dtype(np.int64): lib().oracle_scan_i64}[x.dtype]
+    fn(kind, x.size, _ptr(x), _ptr(out), int(np.array(carry).astype(x.dtype)))
+    return out

@@ -1,0 +1,268 @@
+/* oracle.c — the CPU ORACLE for the GPUArray hot path of arXiv 1304.5553.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_1304_5553_b200/) never imports, links or calls it,
+ * and shares no code, header, table or constant generator with it.
+ *
+ * Plain, slow, obviously correct: ascending-index loops, no blocking, no
+ * fusion, no reordering, no intrinsics.  Built with gcc -O2 -ffp-contract=off
+ * (no -ffast-math, no -march): every float operation below is one IEEE-754
+ * round-to-nearest operation in the type written, with no FMA contraction
+ * (reading R1).
+ *
+ * Passages followed (PAPER.md = /root/reference/PAPER.md):
+ *   elementwise  §3.2.4, PAPER.md:449-458  "a statement ... to be executed for
+ *                each value of i ... All these instances are required to have
+ *                the same length."
+ *   map-reduce   §3.2.5, PAPER.md:460-492  result dtype (471-472), map expression
+ *                over i (473-477), reduction expression over a,b and a neutral
+ *                element (479-485, footnote), scalar result (489-492).
+ *   scan         §3.2.6, PAPER.md:496-499  "parallel prefix sums".
+ * Readings where the paper is silent (rounding sequence, overflow, neutral
+ * elements, NaN, exclusive-scan head, accumulator type) are DESIGN.md R1-R20.
+ *
+ * Parity pins (tests/test_oracle.py): every function here is pinned against
+ * something other than itself — numpy's uncontracted arithmetic, math.fsum,
+ * fractions.Fraction brute force, Python big-int arithmetic, closed forms
+ * (ramp sums, constant-times-ramp dot, all-ones scan) and SPEC.md worked
+ * values.  Exception: the sign of a zero max/min result — "parity unpinned"
+ * (R7; either zero accepted).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stddef.h>
+
+enum { O_F32 = 0, O_F64 = 1, O_I32 = 2, O_I64 = 3 };
+enum { O_SUM = 0, O_MAX = 1, O_MIN = 2 };
+enum { O_MAP_ID = 0, O_MAP_MUL = 1, O_MAP_SQUARE = 2 };
+enum { O_INCLUSIVE = 0, O_EXCLUSIVE = 1 };
+
+/* ------------------------------------------------------------------------ */
+/* Elementwise, §3.2.4.  Statement per index i:           */
+/*   z[i] = a*x[i] + b*y[i]   read as RN(RN(a*x_i) + RN(b*y_i))   (R1)         */
+/*   z[i] = a*x[i] + b        read as RN(RN(a*x_i) + b)                       */
+/* Integers wrap modulo 2^w (R4): computed in unsigned arithmetic.            */
+/* ------------------------------------------------------------------------ */
+void oracle_axpbyz_f32(int64_t n, float a, const float *x, float b, const float *y, float *z) {
+  for (int64_t i = 0; i < n; ++i) {
+    float ax = a * x[i];
+    float by = b * y[i];
+    z[i] = ax + by;
+  }
+}
+
+void oracle_axpbyz_f64(int64_t n, double a, const double *x, double b, const double *y, double *z) {
+  for (int64_t i = 0; i < n; ++i) {
+    double ax = a * x[i];
+    double by = b * y[i];
+    z[i] = ax + by;
+  }
+}
+
+void oracle_axpbyz_i32(int64_t n, int32_t a, const int32_t *x, int32_t b, const int32_t *y, int32_t *z) {
+  for (int64_t i = 0; i < n; ++i) {
+    uint32_t ax = (uint32_t)a * (uint32_t)x[i];
+    uint32_t by = (uint32_t)b * (uint32_t)y[i];
+    z[i] = (int32_t)(ax + by);
+  }
+}
+
+void oracle_axpbyz_i64(int64_t n, int64_t a, const int64_t *x, int64_t b, const int64_t *y, int64_t *z) {
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t ax = (uint64_t)a * (uint64_t)x[i];
+    uint64_t by = (uint64_t)b * (uint64_t)y[i];
+    z[i] = (int64_t)(ax + by);
+  }
+}
+
+void oracle_axpbz_f32(int64_t n, float a, const float *x, float b, float *z) {
+  for (int64_t i = 0; i < n; ++i) {
+    float ax = a * x[i];
+    z[i] = ax + b;
+  }
+}
+
+void oracle_axpbz_f64(int64_t n, double a, const double *x, double b, double *z) {
+  for (int64_t i = 0; i < n; ++i) {
+    double ax = a * x[i];
+    z[i] = ax + b;
+  }
+}
+
+void oracle_axpbz_i32(int64_t n, int32_t a, const int32_t *x, int32_t b, int32_t *z) {
+  for (int64_t i = 0; i < n; ++i) z[i] = (int32_t)((uint32_t)a * (uint32_t)x[i] + (uint32_t)b);
+}
+
+void oracle_axpbz_i64(int64_t n, int64_t a, const int64_t *x, int64_t b, int64_t *z) {
+  for (int64_t i = 0; i < n; ++i) z[i] = (int64_t)((uint64_t)a * (uint64_t)x[i] + (uint64_t)b);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Map-reduce SUM over floats, §3.2.5.                     */
+/* The tree reduction on the GPU approximates the exact real sum of the       */
+/* mapped terms t_i; the oracle computes that sum near-exactly:               */
+/*   map: t_i = x_i | x_i*y_i | x_i*x_i, formed   */
+/*   exactly in float64 (a product of two fp32 values has <= 48 significant   */
+/*   bits).  For fp64 inputs the product p = RN(x*y) and its exact error     */
+/*   e = fma(x, y, -p) are both added, so p + e = x*y exactly.               */
+/*   reduce "a+b", neutral 0: Neumaier-compensated float64 */
+/*   summation in ascending i (BASELINE.json north_star: "reduces in float64  */
+/*   with compensated (Kahan) summation").                                    */
+/* *sumabs receives sum |t_i| (for the n*2^-24*sum|t_i| tolerance clause).    */
+/* ------------------------------------------------------------------------ */
+typedef struct { double s, c; } neumaier_t;
+
+static void neumaier_add(neumaier_t *acc, double t) {
+  double u = acc->s + t;
+  if (fabs(acc->s) >= fabs(t))
+    acc->c += (acc->s - u) + t;
+  else
+    acc->c += (t - u) + acc->s;
+  acc->s = u;
+}
+
+double oracle_sum_f32(int map, int64_t n, const float *x, const float *y, double *sumabs) {
+  neumaier_t acc = {0.0, 0.0};
+  neumaier_t abs_acc = {0.0, 0.0};
+  for (int64_t i = 0; i < n; ++i) {
+    double t;
+    if (map == O_MAP_ID) t = (double)x[i];
+    else if (map == O_MAP_MUL) t = (double)x[i] * (double)y[i];
+    else t = (double)x[i] * (double)x[i];
+    neumaier_add(&acc, t);
+    neumaier_add(&abs_acc, fabs(t));
+  }
+  if (sumabs) *sumabs = abs_acc.s + abs_acc.c;
+  return acc.s + acc.c;
+}
+
+double oracle_sum_f64(int map, int64_t n, const double *x, const double *y, double *sumabs) {
+  neumaier_t acc = {0.0, 0.0};
+  neumaier_t abs_acc = {0.0, 0.0};
+  for (int64_t i = 0; i < n; ++i) {
+    if (map == O_MAP_ID) {
+      neumaier_add(&acc, x[i]);
+      neumaier_add(&abs_acc, fabs(x[i]));
+    } else {
+      double u = x[i];
+      double v = (map == O_MAP_MUL) ? y[i] : x[i];
+      double p = u * v;
+      double e = fma(u, v, -p);
+      neumaier_add(&acc, p);
+      neumaier_add(&acc, e);
+      neumaier_add(&abs_acc, fabs(p));
+    }
+  }
+  if (sumabs) *sumabs = abs_acc.s + abs_acc.c;
+  return acc.s + acc.c;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Map-reduce SUM over integers: "result dtype" is out_dt. */
+/* Inputs are widened to the output width, products and sums wrap modulo     */
+/* 2^w_out (R3, R4).  Returned sign-extended in an int64.                     */
+/* ------------------------------------------------------------------------ */
+static uint64_t load_int(int dt, const void *p, int64_t i) {
+  if (dt == O_I32) return (uint64_t)(int64_t)((const int32_t *)p)[i];
+  return (uint64_t)((const int64_t *)p)[i];
+}
+
+int64_t oracle_sum_int(int map, int in_dt, int out_dt, int64_t n, const void *x, const void *y) {
+  uint64_t s = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t u = load_int(in_dt, x, i);
+    uint64_t t;
+    if (map == O_MAP_ID) t = u;
+    else if (map == O_MAP_MUL) t = u * load_int(in_dt, y, i);
+    else t = u * u;
+    if (out_dt == O_I32) t = (uint64_t)(uint32_t)t;
+    s = s + t;
+    if (out_dt == O_I32) s = (uint64_t)(uint32_t)s;
+  }
+  if (out_dt == O_I32) return (int64_t)(int32_t)(uint32_t)s;
+  return (int64_t)s;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Map-reduce MAX / MIN.  Fold from the neutral element:    */
+/* MAX: -inf / INT_MIN; MIN: +inf / INT_MAX (R5).  The map is evaluated in    */
+/* the input dtype, RN_T(x*y) (R3).  Floats fold with fmax/fmin (maxNum:      */
+/* the non-NaN operand wins, R6).                                             */
+/* ------------------------------------------------------------------------ */
+double oracle_maxmin_f32(int op, int map, int64_t n, const float *x, const float *y) {
+  float acc = (op == O_MAX) ? -INFINITY : INFINITY;
+  for (int64_t i = 0; i < n; ++i) {
+    float t;
+    if (map == O_MAP_ID) t = x[i];
+    else if (map == O_MAP_MUL) t = x[i] * y[i];
+    else t = x[i] * x[i];
+    acc = (op == O_MAX) ? fmaxf(acc, t) : fminf(acc, t);
+  }
+  return (double)acc;
+}
+
+double oracle_maxmin_f64(int op, int map, int64_t n, const double *x, const double *y) {
+  double acc = (op == O_MAX) ? -INFINITY : INFINITY;
+  for (int64_t i = 0; i < n; ++i) {
+    double t;
+    if (map == O_MAP_ID) t = x[i];
+    else if (map == O_MAP_MUL) t = x[i] * y[i];
+    else t = x[i] * x[i];
+    acc = (op == O_MAX) ? fmax(acc, t) : fmin(acc, t);
+  }
+  return acc;
+}
+
+int64_t oracle_maxmin_int(int op, int map, int in_dt, int64_t n, const void *x, const void *y) {
+  int64_t acc;
+  if (in_dt == O_I32) acc = (op == O_MAX) ? (int64_t)INT32_MIN : (int64_t)INT32_MAX;
+  else acc = (op == O_MAX) ? INT64_MIN : INT64_MAX;
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t u = load_int(in_dt, x, i);
+    uint64_t w;
+    if (map == O_MAP_ID) w = u;
+    else if (map == O_MAP_MUL) w = u * load_int(in_dt, y, i);
+    else w = u * u;
+    int64_t t = (in_dt == O_I32) ? (int64_t)(int32_t)(uint32_t)w : (int64_t)w;
+    if (op == O_MAX) { if (t > acc) acc = t; }
+    else { if (t < acc) acc = t; }
+  }
+  return acc;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Scan (prefix sum), §3.2.6, reduction expression "+".    */
+/*   inclusive: y_i = c + x_0 + ... + x_i                                     */
+/*   exclusive: y_0 = c, y_i = c + x_0 + ... + x_{i-1}   (R13)                */
+/* c is the carry-in (0 = the neutral element unless a shard offset is given, */
+/* SURVEY.md §8(a) a7).  Running accumulator in the element type; integers   */
+/* wrap (R4, R14).  out may alias in.                                          */
+/* ------------------------------------------------------------------------ */
+void oracle_scan_i32(int kind, int64_t n, const int32_t *in, int32_t *out, int32_t carry) {
+  uint32_t acc = (uint32_t)carry;
+  for (int64_t i = 0; i < n; ++i) {
+    uint32_t v = (uint32_t)in[i];
+    if (kind == O_INCLUSIVE) {
+      acc = acc + v;
+      out[i] = (int32_t)acc;
+    } else {
+      out[i] = (int32_t)acc;
+      acc = acc + v;
+    }
+  }
+}
+
+void oracle_scan_i64(int kind, int64_t n, const int64_t *in, int64_t *out, int64_t carry) {
+  uint64_t acc = (uint64_t)carry;
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t v = (uint64_t)in[i];
+    if (kind == O_INCLUSIVE) {
+      acc = acc + v;
+      out[i] = (int64_t)acc;
+    } else {
+      out[i] = (int64_t)acc;
+      acc = acc + v;
+    }
+  }
+}
