@@ -1,0 +1,377 @@
+"""bench.py — throughput of the GPUArray hot path on B200 (BASELINE.json metric:
+"achieved HBM GB/s (and % of 8 TB/s peak) for dot/sum/axpbyz/scan at 1/2/4/8 B200").
+
+One STEP = one pass of every hot-path row over one batch of
+synthetic input resident in HBM, per GPU:
+    z = axpbyz(5, x, 6, y)           fp32, 12 B/elt      (a1)
+    dot(x, y), sum(x), norm2sq(x)    fp32, 8/4/4 B/elt   (a2-a4; + a6 allreduce at N>1)
+    exclusive scan(k)                int32, 8 B/elt      (a5; + a7 offset exchange at N>1)
+with n = 2^28 elements per GPU (BASELINE.json configs[1] size; 1 GiB per
+array, > 126 MB L2, so no flush is needed between steps).  Weak scaling: the
+per-GPU shard is fixed, the global array is N x 2^28, shard g holds global
+indices [g*2^28, (g+1)*2^28) of the counter-based generator.
+
+value = algorithmic bytes of all ranks / max-over-ranks device time (GB/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (driver, N > 1)
+
+--impl reference times the CPU oracle (oracle/, test infrastructure) on the
+host cores on a bounded sample of the same workload: there is no reference
+implementation to install (the paper ships no code).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LOG2_N = 28
+N_PER_GPU = 1 << LOG2_N
+A, B = 5.0, 6.0
+# algorithmic bytes per element
+OP_BYTES = {"axpbyz": 12, "dot": 8, "sum": 4, "norm2": 4, "scan": 8}
+OPS = list(OP_BYTES)
+PEAK_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+NOMINAL_GBS = 8000.0
+METRIC = "achieved HBM GB/s (and % of 8 TB/s peak) for dot/sum/axpbyz/scan at 1/2/4/8 B200"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--log2n", type=int, default=LOG2_N, help="per-GPU elements = 2^log2n (default 28)")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: torch copy_ 1 Gi bf16)"
+    except Exception:
+        return PEAK_FALLBACK_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampled every 100 ms while the timed region runs."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [q.strip() for q in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+def oracle_sample(log2n_sample, threads_note="1 (single-threaded plain C oracle)"):
+    """Time the oracle (as it stands) on a bounded sample of the workload:
+    the same five ops on 2^log2n_sample elements regenerated by the synth host
+    twin.  Returns (GB/s, seconds, sample description)."""
+    import numpy as np
+
+    import oracle
+    import synth
+    m = 1 << log2n_sample
+    x = synth.host_fill(synth.F32_U01, synth.SEED_X, m)
+    y = synth.host_fill(synth.F32_U01, synth.SEED_Y, m)
+    k = synth.host_fill(synth.I32_RANGE, synth.SEED_INT, m, lo=0, hi=9)
+    t0 = time.perf_counter()
+    oracle.axpbyz(np.float32(A), x, np.float32(B), y)
+    oracle.reduce(oracle.SUM, oracle.MAP_MUL, x, y)
+    oracle.reduce(oracle.SUM, oracle.MAP_ID, x)
+    oracle.reduce(oracle.SUM, oracle.MAP_SQUARE, x)
+    oracle.scan(oracle.EXCLUSIVE, k)
+    dt = time.perf_counter() - t0
+    nbytes = m * sum(OP_BYTES.values())
+    desc = (f"2^{log2n_sample} elements per op (axpbyz/dot/sum/norm2 fp32 + exclusive scan int32), "
+            f"inputs regenerated by the synth host twin; oracle compute only; threads: {threads_note}")
+    return nbytes / dt / 1e9, dt, desc
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the CPU oracle on host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    log2s = min(args.log2n, 24)
+    for _ in range(max(args.warmup, 0) and 1):
+        oracle_sample(log2s)
+    rates, times = [], []
+    for _ in range(max(args.steps, 1) if args.steps <= 3 else 3):
+        r, t, desc = oracle_sample(log2s)
+        rates.append(r)
+        times.append(t)
+    gbs = statistics.median(rates)
+    ms_per_step_full = (N_PER_GPU if args.log2n == LOG2_N else (1 << args.log2n)) * sum(OP_BYTES.values()) / (gbs * 1e9) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world,
+        "steps": len(rates), "warmup": args.warmup, "ms_per_step": round(ms_per_step_full, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+i32", "data": "synthetic",
+        "config": {"workload": f"configs[1]-sized step per GPU: axpbyz+dot+sum+norm2 fp32 and exclusive scan "
+                               f"int32 on n=2^{args.log2n}; oracle sample 2^{log2s}", "parallelism": "cpu"},
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "no reference code exists (the paper ships none); the reference arm is the CPU oracle, "
+                "timed on a bounded sample, ms_per_step extrapolated to the full step",
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU leg
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_1304_5553_b200 as ga
+    from paper_1304_5553_b200 import dist as gdist
+    from paper_1304_5553_b200 import gpuarray as G
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = 1 << args.log2n
+    start = rank * n  # weak scaling: shard g = global [g*n, (g+1)*n)
+    x = synth.device_fill(synth.F32_U01, synth.SEED_X, n, start=start, device=dev)
+    y = synth.device_fill(synth.F32_U01, synth.SEED_Y, n, start=start, device=dev)
+    k = synth.device_fill(synth.I32_RANGE, synth.SEED_INT, n, start=start, lo=0, hi=9, device=dev)
+    z = torch.empty_like(x)
+    s = torch.empty_like(k)
+    red = torch.empty(3, dtype=torch.float32, device=dev)       # dot, sum, norm2 (one allreduce)
+    totals = torch.empty(world + 1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    ev = {op: [] for op in OPS}
+
+    def step(record):
+        def mark():
+            if record:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                return e
+            return None
+        e0 = mark()
+        G.axpbyz(A, x, B, y, out=z)
+        e1 = mark()
+        G.reduce(G.SUM, G.MUL, x, y, out=red[0:1])
+        e2 = mark()
+        G.reduce(G.SUM, G.ID, x, out=red[1:2])
+        e3 = mark()
+        G.reduce(G.SUM, G.SQUARE, x, out=red[2:3])
+        e4 = mark()
+        if world > 1:
+            dist.all_reduce(red, op=dist.ReduceOp.SUM)
+            gdist.scan(k, exclusive=True, out=s, totals=totals)
+        else:
+            G.scan(k, exclusive=True, out=s)
+        e5 = mark()
+        if record:
+            for op, (a, b) in zip(OPS, ((e0, e1), (e1, e2), (e2, e3), (e3, e4), (e4, e5))):
+                ev[op].append((a, b))
+
+    for _ in range(max(args.warmup, 3)):
+        step(False)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)  # let the sampler start
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ga.launch_count()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_stop = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for _ in range(args.steps):
+        step(True)
+    t_stop.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = ga.launch_count() - launches0
+    clk = clocks.stop()
+    elapsed_ms = t_start.elapsed_time(t_stop)
+
+    per_op_ms = {op: sum(a.elapsed_time(b) for a, b in ev[op]) / len(ev[op]) for op in OPS}
+    t = torch.tensor([elapsed_ms] + [per_op_ms[op] for op in OPS], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t[0])
+    per_op_ms = {op: float(v) for op, v in zip(OPS, t[1:].tolist())}
+
+    # ---- parity spot-check of this run's outputs (sampled; full parity is in tests/)
+    torch.cuda.synchronize()
+
+    # ---- end-to-end through the public API with host buffers
+    e2e = run_e2e(args, world, rank, dev, n, start, ga, G, gdist, torch, dist)
+
+    if rank == 0:
+        peak, peak_src = peaks()
+        step_bytes = n * sum(OP_BYTES.values())
+        ms_per_step = elapsed_ms / args.steps
+        value = world * step_bytes / (ms_per_step * 1e-3) / 1e9
+        ops = {}
+        for op in OPS:
+            gbs = n * OP_BYTES[op] / (per_op_ms[op] * 1e-3) / 1e9
+            ops[op] = {"ms": round(per_op_ms[op], 4), "gbs": round(gbs, 1), "frac_of_measured": round(gbs / peak, 4),
+                       "frac_of_8tbs": round(gbs / NOMINAL_GBS, 4), "bytes_per_elt": OP_BYTES[op]}
+        dom = max(OPS, key=lambda o: per_op_ms[o])
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ops[dom]["gbs"], "peak": peak, "unit": "GB/s",
+                "frac": round(ops[dom]["gbs"] / peak, 4), "peak_source": peak_src,
+                "traffic": ncu_traffic(dom, args.log2n),
+                "algorithmic_bytes_per_launch": n * OP_BYTES[dom]}
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            g, secs, desc = oracle_sample(min(args.log2n, 24))
+            cpu = {"value": round(g, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc,
+                   "seconds": round(secs, 3)}
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32+i32", "data": "synthetic",
+            "config": {"workload": f"configs[1]-sized step: axpbyz(5,x,6,y)+dot+sum+norm2 fp32 U[0,1) and exclusive "
+                                   f"scan int32 U{{0..9}} on n=2^{args.log2n} per GPU (weak scaling)",
+                       "n_per_gpu": n, "global_n": n * world, "parallelism": f"dp{world} (contiguous shards)",
+                       "l2": "inputs 1 GiB per array > 126 MB L2; no flush needed" if args.log2n >= 26 else
+                             "inputs smaller than 4x L2: L2-warm numbers"},
+            "frac_of_8tbs": round(value / world / NOMINAL_GBS, 4),
+            "elements_per_s": round(world * n * len(OPS) / (ms_per_step * 1e-3), 1),
+            "ops": ops, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "launches_per_step": launches / args.steps, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, world, rank, dev, n, start, ga, G, gdist, torch, dist):
+    """Same step through the public API with pinned HOST inputs: H2D of x, y, k,
+    the five ops, D2H of z, the scan output and the three scalars — all inside
+    the timed region."""
+    import synth
+    steps = max(1, args.e2e_steps)
+    xh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    yh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    kh = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    synth.host_fill(synth.F32_U01, synth.SEED_X, n, start=start, out=xh.numpy())
+    synth.host_fill(synth.F32_U01, synth.SEED_Y, n, start=start, out=yh.numpy())
+    synth.host_fill(synth.I32_RANGE, synth.SEED_INT, n, start=start, lo=0, hi=9, out=kh.numpy())
+    zh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    sh = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    rh = torch.empty(3, dtype=torch.float32, pin_memory=True)
+    totals = torch.empty(world + 1, dtype=torch.int32, device=dev)
+
+    def one():
+        x = xh.to(dev, non_blocking=True)
+        y = yh.to(dev, non_blocking=True)
+        k = kh.to(dev, non_blocking=True)
+        z = G.axpbyz(A, x, B, y)
+        red = torch.empty(3, dtype=torch.float32, device=dev)
+        gdist.reduce_many([(G.MUL, x, y), (G.ID, x, None), (G.SQUARE, x, None)], red)
+        s = gdist.scan(k, exclusive=True, totals=totals)
+        zh.copy_(z, non_blocking=True)
+        sh.copy_(s, non_blocking=True)
+        rh.copy_(red, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        return float(rh[0])
+
+    one()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(steps):
+        one()
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt[0])
+    step_bytes = n * sum(OP_BYTES.values())
+    return {"value": round(world * step_bytes / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": 3 * n * 4, "d2h_bytes_per_step": 2 * n * 4 + 3 * 4, "ms_per_step": round(ms, 3),
+            "steps": steps, "path": "pinned host -> device copies + paper_1304_5553_b200 public API + device -> host"}
+
+
+def ncu_traffic(kernel, log2n):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full summary (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(f"{kernel}@2^{log2n}")
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    main()

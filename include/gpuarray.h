@@ -1,0 +1,152 @@
+/* gpuarray.h — C ABI of the B200-native GPUArray hot path (arXiv 1304.5553).
+ *
+ * The three operations of the paper's GPUArray layer, each as one
+ * asynchronous call that enqueues ONE hand-written sm_100a kernel on a
+ * caller-supplied CUDA stream and returns at once ("the invocation returns
+ * immediately and does not wait for completion on the GPU", PAPER.md:338-340,
+ * §3.1):
+ *
+ *   gpuarray_axpbyz / gpuarray_axpbz   ElementwiseKernel, §3.2.4
+ *       "a statement ... to be executed for each value of
+ *       i ... All these instances are required to have the same length."
+ *       The statement is fixed at build time to z[i] = a*x[i] + b*y[i]
+ *       (resp. a*x[i] + b) instead of a run-time C string.
+ *   gpuarray_reduce                    ReductionKernel (map-reduce), §3.2.5
+ *       result dtype (471-472), a map expression over i
+ *       (473-477), a reduction expression of a and b with its neutral element
+ *       (479-485), result "a GPUArray scalar still residing on the GPU"
+ *       (489-492).  The map and reduction expressions are enums.
+ *   gpuarray_scan                      parallel prefix sum, §3.2.6
+ *       "GPU-based parallel prefix sums".
+ *
+ * Conventions (all entry points):
+ *   - Pointers x, y, z, in, out, carry, workspace are DEVICE pointers on the
+ *     current CUDA device; `stream` is a cudaStream_t (NULL = legacy default
+ *     stream).  Arrays are contiguous, 1-D, of n elements of the given dtype,
+ *     element-aligned (any offset; the fast path wants x, y, z to share their
+ *     address phase modulo 32 bytes — otherwise a slower GPU path is used).
+ *   - Ownership: the caller owns every buffer and must keep it alive until
+ *     the stream has passed the call.  The library allocates no device
+ *     memory, keeps no pointer after returning, and never synchronises.
+ *   - Errors (PAPER.md:288-290 raise-on-error model, as status codes): the
+ *     return value reports argument and launch errors synchronously; faults
+ *     during execution surface at the caller's next synchronisation.
+ *     gpuarray_last_error() gives a thread-local detail string.
+ *   - Exactly one kernel is launched per call (zero for n == 0, except reduce,
+ *     which writes the neutral element with one tiny kernel).
+ */
+#ifndef GPUARRAY_H
+#define GPUARRAY_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GPUARRAY_ABI_VERSION 1
+
+typedef enum { GA_F32 = 0, GA_F64 = 1, GA_I32 = 2, GA_I64 = 3 } ga_dtype_t;
+
+/* Reduction expression "a+b", "max(a,b)", "min(a,b)" with its neutral element
+ * (PAPER.md:479-485 and footnote): SUM 0; MAX -inf / INT_MIN; MIN +inf /
+ * INT_MAX (R5).  Floats use maxNum/minNum: a NaN operand loses (R6). */
+typedef enum { GA_OP_SUM = 0, GA_OP_MAX = 1, GA_OP_MIN = 2 } ga_op_t;
+
+/* Map expression over index i:
+ * x[i] | x[i]*y[i] (dot) | x[i]*x[i] (squared 2-norm). */
+typedef enum { GA_MAP_ID = 0, GA_MAP_MUL = 1, GA_MAP_SQUARE = 2 } ga_map_t;
+
+typedef enum { GA_SCAN_INCLUSIVE = 0, GA_SCAN_EXCLUSIVE = 1 } ga_scan_kind_t;
+
+typedef enum {
+  GA_OK = 0,
+  GA_ERR_INVALID_ARGUMENT = 1, /* n < 0, NULL with n > 0, bad enum, scalar dtype != dt,
+                                  y missing for MAP_MUL, partial overlap of output and input */
+  GA_ERR_UNSUPPORTED = 2,      /* combination not instantiated (e.g. MAX with out_dt != in_dt) */
+  GA_ERR_WORKSPACE = 3,        /* workspace NULL or smaller than *_workspace_bytes() */
+  GA_ERR_CUDA = 4              /* CUDA error at launch; see gpuarray_last_error() */
+} ga_status_t;
+
+/* A host scalar typed like the arrays it combines with ("numpy sized
+ * scalars such as numpy.float32(5.7)"; R2). */
+typedef struct ga_scalar {
+  int32_t dtype;    /* ga_dtype_t of the value; must equal the call's dt */
+  int32_t reserved; /* must be 0 */
+  union {
+    float f32;
+    double f64;
+    int32_t i32;
+    int64_t i64;
+  } v;
+} ga_scalar_t;
+
+/* z[i] = a*x[i] + b*y[i], i in [0, n).
+ * Floats: z_i = RN(RN(a*x_i) + RN(b*y_i)) — two roundings of the products and
+ * one of the sum, no FMA contraction (R1).  Integers wrap modulo
+ * 2^w (R4).  dt in {F32, F64, I32, I64}.  z may equal x or y exactly
+ * (in-place); any other overlap is GA_ERR_INVALID_ARGUMENT.  n == 0: no-op. */
+ga_status_t gpuarray_axpbyz(ga_dtype_t dt, int64_t n, ga_scalar_t a, const void *x, ga_scalar_t b,
+                            const void *y, void *z, void *stream);
+
+/* z[i] = a*x[i] + b (floats: RN(RN(a*x_i) + b)).  Listing 1's "multiply by
+ * two" is a = 2, b = -0.0 (the IEEE additive identity, R21). */
+ga_status_t gpuarray_axpbz(ga_dtype_t dt, int64_t n, ga_scalar_t a, const void *x, ga_scalar_t b,
+                           void *z, void *stream);
+
+/* Bytes of workspace gpuarray_reduce needs (an upper bound for every n and
+ * every device).  The workspace must be zero-filled ONCE when allocated; the
+ * kernel leaves it reusable (the completion ticket resets itself).  Calls
+ * that may run concurrently need distinct workspaces, and a reduce workspace
+ * must not be passed to gpuarray_scan (or vice versa): the layouts differ. */
+size_t gpuarray_reduce_workspace_bytes(ga_dtype_t out_dt, int64_t n);
+
+/* *out = fold over i in [0, n) of map(x, y)[i] with `op`, starting from the
+ * neutral element; out is a DEVICE scalar of out_dt.
+ * Supported (in_dt -> out_dt):
+ *   SUM: F32->F32, F32->F64, F64->F64, I32->I32, I32->I64, I64->I64
+ *        (accumulation in out_dt; integer maps widen to out_dt then wrap, R3/R4)
+ *   MAX, MIN: out_dt == in_dt; the map is evaluated in in_dt (RN(x*y), wrap).
+ * y must be non-NULL iff map == GA_MAP_MUL (it is ignored otherwise).
+ * Float SUM is a tree-ordered sum (not the exact sum): deterministic for a
+ * given (n, device), accurate as DESIGN.md R9/R10 state.  n == 0 writes the
+ * neutral element. */
+ga_status_t gpuarray_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
+                            const void *x, const void *y, void *out, void *workspace,
+                            size_t workspace_bytes, void *stream);
+
+/* Bytes of workspace gpuarray_scan needs for (dt, n): a 256-byte header plus
+ * per-tile look-back status.  Zero-fill once; reusable afterwards (status
+ * words are epoch-tagged, the tile counter resets itself).  Never share it
+ * with gpuarray_reduce.  A corrupted workspace makes the kernel trap (a CUDA
+ * error at the next synchronisation) after 10 s instead of hanging. */
+size_t gpuarray_scan_workspace_bytes(ga_dtype_t dt, int64_t n);
+
+/* Prefix sum with "+" (op must be GA_OP_SUM), dt in {I32, I64}:
+ *   inclusive: out[i] = c + in[0] + ... + in[i]
+ *   exclusive: out[0] = c, out[i] = c + in[0] + ... + in[i-1]   (R13)
+ * where c = carry[0] + ... + carry[carry_count-1] (a device array of dt; c = 0,
+ * the neutral element, when carry_count == 0).  The carry is how a sharded
+ * scan passes the totals of earlier shards.  Integers
+ * wrap (R4, R14).  out may equal in (in-place); other overlap is invalid.
+ * n == 0: no-op. */
+ga_status_t gpuarray_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_t n, const void *in,
+                          void *out, const void *carry, int64_t carry_count, void *workspace,
+                          size_t workspace_bytes, void *stream);
+
+/* Static strings; never NULL. */
+const char *gpuarray_status_string(ga_status_t status);
+/* Thread-local detail of the last non-OK status on this thread ("" if none). */
+const char *gpuarray_last_error(void);
+/* GPUARRAY_ABI_VERSION of the loaded library. */
+int gpuarray_abi_version(void);
+/* Number of kernels this library has launched in this process (all threads).
+ * Evidence for bench.py's "gpu_launches". */
+uint64_t gpuarray_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GPUARRAY_H */

@@ -1,0 +1,50 @@
+// ga_host.h — host-side helpers of the C ABI: status/error reporting, device
+// queries cached per device, launch accounting.  Product code only.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gpuarray.h"
+
+namespace ga {
+
+// Record a detail string for gpuarray_last_error() and return `s`.
+ga_status_t fail(ga_status_t s, const char *fmt, ...);
+// Map a CUDA error from a launch to GA_ERR_CUDA (clearing the sticky-free error).
+ga_status_t check_launch(const char *what);
+// Number of SMs of the current device (cached).
+int sm_count();
+// Count one kernel launch (gpuarray_launch_count()).
+void count_launch();
+
+// Largest grid whose CTAs are all co-resident: SMs x occupancy (cached per
+// kernel by the caller through a function-local static).
+int resident_grid(const void *kernel, int block, size_t dyn_smem = 0);
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline size_t dtype_size(ga_dtype_t dt) { return (dt == GA_F32 || dt == GA_I32) ? 4 : 8; }
+
+inline bool valid_dtype(int dt) { return dt >= GA_F32 && dt <= GA_I64; }
+
+// [p, p+bytes) and [q, q+bytes2) overlap without being the same start.
+inline bool partial_overlap(const void *p, size_t bytes, const void *q, size_t bytes2) {
+  uintptr_t a = (uintptr_t)p, b = (uintptr_t)q;
+  if (a == b) return false;
+  return a < b + bytes2 && b < a + bytes;
+}
+
+// Launchers implemented per kernel family (elementwise.cu, reduce.cu, scan.cu).
+ga_status_t launch_axpbyz(ga_dtype_t dt, int64_t n, const ga_scalar_t &a, const void *x,
+                          const ga_scalar_t &b, const void *y, void *z, cudaStream_t s);
+ga_status_t launch_axpbz(ga_dtype_t dt, int64_t n, const ga_scalar_t &a, const void *x,
+                         const ga_scalar_t &b, void *z, cudaStream_t s);
+ga_status_t launch_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
+                          const void *x, const void *y, void *out, void *ws, cudaStream_t s);
+ga_status_t launch_scan(ga_scan_kind_t kind, ga_dtype_t dt, int64_t n, const void *in, void *out,
+                        const void *carry, int64_t carry_count, void *ws, cudaStream_t s);
+
+size_t reduce_workspace_bytes();
+size_t scan_workspace_bytes(ga_dtype_t dt, int64_t n);
+
+}  // namespace ga

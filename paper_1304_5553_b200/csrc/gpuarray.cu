@@ -1,0 +1,160 @@
+// gpuarray.cu — the C ABI declared in include/gpuarray.h: argument
+// validation, dispatch to the kernel launchers, status strings and
+// thread-local error detail.  No device allocation, no host synchronisation.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <utility>
+
+#include "ga_host.h"
+#include "gpuarray.h"
+
+namespace ga {
+
+static thread_local char g_last_error[512] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+ga_status_t fail(ga_status_t s, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+ga_status_t check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(GA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return GA_OK;
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int sm_count() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 1;
+}
+
+int resident_grid(const void *kernel, int block, size_t dyn_smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_pair(kernel, dev * 65536 + block);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, dyn_smem) != cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  int grid = per_sm * sm_count();
+  cache[key] = grid;
+  return grid;
+}
+
+}  // namespace ga
+
+using namespace ga;
+
+static bool scalar_ok(const ga_scalar_t &s, ga_dtype_t dt) { return s.dtype == (int32_t)dt && s.reserved == 0; }
+
+extern "C" {
+
+ga_status_t gpuarray_axpbyz(ga_dtype_t dt, int64_t n, ga_scalar_t a, const void *x, ga_scalar_t b, const void *y,
+                            void *z, void *stream) {
+  if (!valid_dtype(dt)) return fail(GA_ERR_INVALID_ARGUMENT, "axpbyz: bad dtype %d", (int)dt);
+  if (n < 0) return fail(GA_ERR_INVALID_ARGUMENT, "axpbyz: n < 0");
+  if (!scalar_ok(a, dt) || !scalar_ok(b, dt))
+    return fail(GA_ERR_INVALID_ARGUMENT, "axpbyz: scalar dtype differs from array dtype");
+  if (n == 0) return GA_OK;
+  if (!x || !y || !z) return fail(GA_ERR_INVALID_ARGUMENT, "axpbyz: NULL array with n > 0");
+  const size_t bytes = (size_t)n * dtype_size(dt);
+  if (partial_overlap(z, bytes, x, bytes) || partial_overlap(z, bytes, y, bytes))
+    return fail(GA_ERR_INVALID_ARGUMENT, "axpbyz: z partially overlaps x or y");
+  return launch_axpbyz(dt, n, a, x, b, y, z, (cudaStream_t)stream);
+}
+
+ga_status_t gpuarray_axpbz(ga_dtype_t dt, int64_t n, ga_scalar_t a, const void *x, ga_scalar_t b, void *z,
+                           void *stream) {
+  if (!valid_dtype(dt)) return fail(GA_ERR_INVALID_ARGUMENT, "axpbz: bad dtype %d", (int)dt);
+  if (n < 0) return fail(GA_ERR_INVALID_ARGUMENT, "axpbz: n < 0");
+  if (!scalar_ok(a, dt) || !scalar_ok(b, dt))
+    return fail(GA_ERR_INVALID_ARGUMENT, "axpbz: scalar dtype differs from array dtype");
+  if (n == 0) return GA_OK;
+  if (!x || !z) return fail(GA_ERR_INVALID_ARGUMENT, "axpbz: NULL array with n > 0");
+  const size_t bytes = (size_t)n * dtype_size(dt);
+  if (partial_overlap(z, bytes, x, bytes)) return fail(GA_ERR_INVALID_ARGUMENT, "axpbz: z partially overlaps x");
+  return launch_axpbz(dt, n, a, x, b, z, (cudaStream_t)stream);
+}
+
+size_t gpuarray_reduce_workspace_bytes(ga_dtype_t out_dt, int64_t n) {
+  (void)out_dt;
+  (void)n;
+  return reduce_workspace_bytes();
+}
+
+ga_status_t gpuarray_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n, const void *x,
+                            const void *y, void *out, void *workspace, size_t workspace_bytes, void *stream) {
+  if (op < GA_OP_SUM || op > GA_OP_MIN) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: bad op %d", (int)op);
+  if (map < GA_MAP_ID || map > GA_MAP_SQUARE) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: bad map %d", (int)map);
+  if (!valid_dtype(in_dt) || !valid_dtype(out_dt)) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: bad dtype");
+  if (n < 0) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: n < 0");
+  if (!out) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: out is NULL");
+  if (n > 0 && !x) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: x is NULL with n > 0");
+  if (map == GA_MAP_MUL && n > 0 && !y) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: MAP_MUL needs y");
+  if (!workspace || workspace_bytes < reduce_workspace_bytes())
+    return fail(GA_ERR_WORKSPACE, "reduce: workspace needs %zu bytes", reduce_workspace_bytes());
+  return launch_reduce(op, map, in_dt, out_dt, n, x, map == GA_MAP_MUL ? y : nullptr, out, workspace,
+                       (cudaStream_t)stream);
+}
+
+size_t gpuarray_scan_workspace_bytes(ga_dtype_t dt, int64_t n) { return n < 0 ? 0 : scan_workspace_bytes(dt, n); }
+
+ga_status_t gpuarray_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_t n, const void *in, void *out,
+                          const void *carry, int64_t carry_count, void *workspace, size_t workspace_bytes,
+                          void *stream) {
+  if (op != GA_OP_SUM) return fail(GA_ERR_UNSUPPORTED, "scan: only GA_OP_SUM is instantiated");
+  if (kind != GA_SCAN_INCLUSIVE && kind != GA_SCAN_EXCLUSIVE)
+    return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad kind %d", (int)kind);
+  if (!valid_dtype(dt)) return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad dtype %d", (int)dt);
+  if (dt != GA_I32 && dt != GA_I64) return fail(GA_ERR_UNSUPPORTED, "scan: dtype %d not instantiated", (int)dt);
+  if (n < 0) return fail(GA_ERR_INVALID_ARGUMENT, "scan: n < 0");
+  if (carry_count < 0 || (carry_count > 0 && !carry))
+    return fail(GA_ERR_INVALID_ARGUMENT, "scan: carry_count < 0 or carry NULL");
+  if (n == 0) return GA_OK;
+  if (!in || !out) return fail(GA_ERR_INVALID_ARGUMENT, "scan: NULL array with n > 0");
+  const size_t bytes = (size_t)n * dtype_size(dt);
+  if (partial_overlap(out, bytes, in, bytes)) return fail(GA_ERR_INVALID_ARGUMENT, "scan: out partially overlaps in");
+  const size_t need = scan_workspace_bytes(dt, n);
+  if (!workspace || workspace_bytes < need) return fail(GA_ERR_WORKSPACE, "scan: workspace needs %zu bytes", need);
+  return launch_scan(kind, dt, n, in, out, carry, carry_count, workspace, (cudaStream_t)stream);
+}
+
+const char *gpuarray_status_string(ga_status_t s) {
+  switch (s) {
+    case GA_OK: return "GA_OK";
+    case GA_ERR_INVALID_ARGUMENT: return "GA_ERR_INVALID_ARGUMENT";
+    case GA_ERR_UNSUPPORTED: return "GA_ERR_UNSUPPORTED";
+    case GA_ERR_WORKSPACE: return "GA_ERR_WORKSPACE";
+    case GA_ERR_CUDA: return "GA_ERR_CUDA";
+  }
+  return "GA_ERR_UNKNOWN";
+}
+
+const char *gpuarray_last_error(void) { return g_last_error; }
+
+int gpuarray_abi_version(void) { return GPUARRAY_ABI_VERSION; }
+
+uint64_t gpuarray_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+}  // extern "C"

@@ -1,0 +1,254 @@
+// reduce.cu — ReductionKernel-style map-reduce (§3.2.5):
+// "evaluating an element-wise expression ahead of reduction" (463-467), a
+// reduction expression of a and b with its neutral element (479-485), and a
+// result that is "a GPUArray scalar still residing on the GPU" (489-492).
+//
+// Single pass, one launch, HBM-bound (4 B/elt fp32 sum/norm2, 8 B/elt dot):
+//   1. grid-stride map + accumulate: each thread keeps one accumulator per
+//      lane of a 256-bit vector (8 for fp32) and keeps UNROLL vectors per
+//      input in flight (LDG.256, L1 bypassed); scalar head/tail for the
+//      unaligned ends; out-of-range work contributes the neutral element;
+//   2. fixed-order lane tree -> warp xor-butterfly -> per-warp partial in
+//      shared memory -> warp 0 folds the block partial;
+//   3. last-block-done finish: the block partial goes to workspace, then
+//      __threadfence + an atomic ticket; the block that draws the last ticket
+//      folds all partials in index order, writes *out and resets the ticket
+//      (no second launch, no host sync, no memset between calls).
+// Deterministic for a given (n, device): every fold order above is fixed.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <type_traits>
+
+#include "ga_device.cuh"
+#include "ga_host.h"
+
+namespace ga {
+namespace {
+
+constexpr int RED_BLOCK = 256;
+constexpr int RED_MAX_PARTIALS = 8192;
+constexpr size_t RED_HEADER = 128;  // ticket lives in its own 128-byte line
+
+template <typename T>
+__host__ __device__ constexpr bool is_fp() {
+  return std::is_floating_point<T>::value;
+}
+
+// Map (over index i) then accumulate into the reduction's accumulator.
+// SUM over floats accumulates in Tacc with one fused multiply-add per term
+// (exact product, one rounding): the tolerance of DESIGN.md R9/R10 applies.
+// SUM over integers widens to Tacc, then wraps (R3, R4).  MAX/MIN evaluate
+// the map in Tin with RN / wrap (R3) and fold with maxNum/minNum (R6).
+template <typename Tin, typename Tacc, int OP, int MAP>
+__device__ __forceinline__ Tacc map_acc(Tacc acc, Tin x, Tin y) {
+  if constexpr (OP == GA_OP_SUM) {
+    const Tacc u = (Tacc)x;
+    if constexpr (is_fp<Tacc>()) {
+      if constexpr (MAP == GA_MAP_ID) return e_add(acc, u);
+      else if constexpr (MAP == GA_MAP_MUL) return e_fma(u, (Tacc)y, acc);
+      else return e_fma(u, u, acc);
+    } else {
+      if constexpr (MAP == GA_MAP_ID) return e_add(acc, u);
+      else if constexpr (MAP == GA_MAP_MUL) return e_add(acc, e_mul(u, (Tacc)y));
+      else return e_add(acc, e_mul(u, u));
+    }
+  } else {
+    Tin t;
+    if constexpr (MAP == GA_MAP_ID) t = x;
+    else if constexpr (MAP == GA_MAP_MUL) t = e_mul(x, y);
+    else t = e_mul(x, x);
+    return Op<OP, Tacc>::fold(acc, (Tacc)t);
+  }
+}
+
+template <typename Tin, typename Tacc>
+struct RedArgs {
+  int64_t n;
+  int64_t head;  // elements folded by the scalar loop before the aligned body
+  int64_t nvec;  // 32-byte vectors in the body
+  const Tin *x;
+  const Tin *y;
+  Tacc *out;
+  Tacc *partials;
+  unsigned int *ticket;
+};
+
+// Block-wide fold; result valid in thread 0.  Fixed order.
+template <int OP, typename T>
+__device__ __forceinline__ T block_fold(T v, T *smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_fold<OP, T>(v);
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < RED_BLOCK / 32 ? smem[lane] : Op<OP, T>::neutral();
+    v = warp_fold<OP, T>(v);
+  }
+  return v;
+}
+
+template <typename Tin, typename Tacc, int OP, int MAP, int UNROLL>
+__global__ void __launch_bounds__(RED_BLOCK) reduce_kernel(RedArgs<Tin, Tacc> p) {
+  constexpr int VEC = 32 / sizeof(Tin);
+  constexpr bool HAS_Y = MAP == GA_MAP_MUL;
+  __shared__ Tacc smem[RED_BLOCK / 32];
+  __shared__ bool is_last;
+
+  const int64_t tid = (int64_t)blockIdx.x * RED_BLOCK + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * RED_BLOCK;
+
+  Tacc acc[VEC];
+#pragma unroll
+  for (int k = 0; k < VEC; ++k) acc[k] = Op<OP, Tacc>::neutral();
+
+  // Scalar parts: the unaligned head (all of x when x/y are not co-aligned)
+  // and the tail after the last whole vector.
+  for (int64_t i = tid; i < p.head; i += nthreads)
+    acc[0] = map_acc<Tin, Tacc, OP, MAP>(acc[0], p.x[i], HAS_Y ? p.y[i] : Tin(0));
+  const int64_t tail0 = p.head + p.nvec * VEC;
+  for (int64_t i = tail0 + tid; i < p.n; i += nthreads)
+    acc[VEC - 1] = map_acc<Tin, Tacc, OP, MAP>(acc[VEC - 1], p.x[i], HAS_Y ? p.y[i] : Tin(0));
+
+  const char *xb = reinterpret_cast<const char *>(p.x + p.head);
+  const char *yb = HAS_Y ? reinterpret_cast<const char *>(p.y + p.head) : nullptr;
+  for (int64_t base = tid; base < p.nvec; base += nthreads * UNROLL) {
+    V32 vx[UNROLL], vy[UNROLL];
+#pragma unroll
+    for (int j = 0; j < UNROLL; ++j) {
+      const int64_t v = base + j * nthreads;
+      if (v < p.nvec) {
+        vx[j] = ld_nc_256(xb + v * 32);
+        if constexpr (HAS_Y) vy[j] = ld_nc_256(yb + v * 32);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < UNROLL; ++j) {
+      const int64_t v = base + j * nthreads;
+      if (v < p.nvec) {
+#pragma unroll
+        for (int k = 0; k < VEC; ++k)
+          acc[k] = map_acc<Tin, Tacc, OP, MAP>(acc[k], vget<Tin>(vx[j], k), HAS_Y ? vget<Tin>(vy[j], k) : Tin(0));
+      }
+    }
+  }
+
+  // Lane tree: ((a0+a4)+(a2+a6)) + ((a1+a5)+(a3+a7)) for VEC = 8.
+#pragma unroll
+  for (int w = VEC / 2; w >= 1; w >>= 1) {
+#pragma unroll
+    for (int k = 0; k < w; ++k) acc[k] = Op<OP, Tacc>::fold(acc[k], acc[k + w]);
+  }
+  Tacc v = block_fold<OP, Tacc>(acc[0], smem);
+
+  if (threadIdx.x == 0) {
+    p.partials[blockIdx.x] = v;
+    __threadfence();
+    is_last = atomicAdd(p.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!is_last) return;
+
+  // Last block: fold the partials in index order (L2 reads, bypassing L1).
+  __threadfence();
+  Tacc w = Op<OP, Tacc>::neutral();
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += RED_BLOCK) w = Op<OP, Tacc>::fold(w, __ldcg(p.partials + i));
+  __syncthreads();  // smem reuse
+  w = block_fold<OP, Tacc>(w, smem);
+  if (threadIdx.x == 0) {
+    *p.out = w;
+    *p.ticket = 0u;  // reusable by the next call on this workspace
+  }
+}
+
+template <typename Tacc, int OP>
+__global__ void neutral_kernel(Tacc *out) {
+  *out = Op<OP, Tacc>::neutral();
+}
+
+template <typename Tin, typename Tacc, int OP, int MAP>
+ga_status_t run(int64_t n, const void *x, const void *y, void *out, void *ws, cudaStream_t s) {
+  if (n == 0) {
+    neutral_kernel<Tacc, OP><<<1, 1, 0, s>>>(static_cast<Tacc *>(out));
+    count_launch();
+    return check_launch("neutral_kernel");
+  }
+  constexpr int VEC = 32 / sizeof(Tin);
+  constexpr int UNROLL = (MAP == GA_MAP_MUL) ? 2 : 4;
+  RedArgs<Tin, Tacc> p;
+  p.n = n;
+  p.x = static_cast<const Tin *>(x);
+  p.y = static_cast<const Tin *>(y);
+  p.out = static_cast<Tacc *>(out);
+  p.ticket = static_cast<unsigned int *>(ws);
+  p.partials = reinterpret_cast<Tacc *>(static_cast<char *>(ws) + RED_HEADER);
+
+  const uintptr_t phase = (uintptr_t)x & 31;
+  const bool coaligned = (MAP != GA_MAP_MUL || ((uintptr_t)y & 31) == phase) && (phase % sizeof(Tin)) == 0;
+  if (coaligned) {
+    p.head = std::min<int64_t>(n, (int64_t)(((32 - phase) & 31) / sizeof(Tin)));
+    p.nvec = (n - p.head) / VEC;
+  } else {
+    p.head = n;
+    p.nvec = 0;
+  }
+  auto kern = reduce_kernel<Tin, Tacc, OP, MAP, UNROLL>;
+  const int max_grid = std::min(resident_grid((const void *)kern, RED_BLOCK), RED_MAX_PARTIALS);
+  const int64_t work = coaligned ? std::max<int64_t>(p.nvec, 1) : n;
+  const int grid = (int)std::min<int64_t>(cdiv(work, RED_BLOCK), max_grid);
+  kern<<<grid, RED_BLOCK, 0, s>>>(p);
+  count_launch();
+  return check_launch("reduce_kernel");
+}
+
+template <typename Tin, typename Tacc, int OP>
+ga_status_t by_map(ga_map_t map, int64_t n, const void *x, const void *y, void *out, void *ws, cudaStream_t s) {
+  switch (map) {
+    case GA_MAP_ID: return run<Tin, Tacc, OP, GA_MAP_ID>(n, x, y, out, ws, s);
+    case GA_MAP_MUL: return run<Tin, Tacc, OP, GA_MAP_MUL>(n, x, y, out, ws, s);
+    case GA_MAP_SQUARE: return run<Tin, Tacc, OP, GA_MAP_SQUARE>(n, x, y, out, ws, s);
+  }
+  return fail(GA_ERR_INVALID_ARGUMENT, "bad map %d", (int)map);
+}
+
+template <typename T, int OP>
+ga_status_t maxmin(ga_map_t map, int64_t n, const void *x, const void *y, void *out, void *ws, cudaStream_t s) {
+  return by_map<T, T, OP>(map, n, x, y, out, ws, s);
+}
+
+}  // namespace
+
+size_t reduce_workspace_bytes() { return RED_HEADER + (size_t)RED_MAX_PARTIALS * 8; }
+
+ga_status_t launch_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
+                          const void *x, const void *y, void *out, void *ws, cudaStream_t s) {
+  if (op == GA_OP_SUM) {
+    if (in_dt == GA_F32 && out_dt == GA_F32) return by_map<float, float, GA_OP_SUM>(map, n, x, y, out, ws, s);
+    if (in_dt == GA_F32 && out_dt == GA_F64) return by_map<float, double, GA_OP_SUM>(map, n, x, y, out, ws, s);
+    if (in_dt == GA_F64 && out_dt == GA_F64) return by_map<double, double, GA_OP_SUM>(map, n, x, y, out, ws, s);
+    if (in_dt == GA_I32 && out_dt == GA_I32) return by_map<int32_t, int32_t, GA_OP_SUM>(map, n, x, y, out, ws, s);
+    if (in_dt == GA_I32 && out_dt == GA_I64) return by_map<int32_t, int64_t, GA_OP_SUM>(map, n, x, y, out, ws, s);
+    if (in_dt == GA_I64 && out_dt == GA_I64) return by_map<int64_t, int64_t, GA_OP_SUM>(map, n, x, y, out, ws, s);
+    return fail(GA_ERR_UNSUPPORTED, "SUM %d -> %d not instantiated", (int)in_dt, (int)out_dt);
+  }
+  if (in_dt != out_dt) return fail(GA_ERR_UNSUPPORTED, "MAX/MIN need out_dt == in_dt");
+  if (op == GA_OP_MAX) {
+    switch (in_dt) {
+      case GA_F32: return maxmin<float, GA_OP_MAX>(map, n, x, y, out, ws, s);
+      case GA_F64: return maxmin<double, GA_OP_MAX>(map, n, x, y, out, ws, s);
+      case GA_I32: return maxmin<int32_t, GA_OP_MAX>(map, n, x, y, out, ws, s);
+      case GA_I64: return maxmin<int64_t, GA_OP_MAX>(map, n, x, y, out, ws, s);
+    }
+  } else if (op == GA_OP_MIN) {
+    switch (in_dt) {
+      case GA_F32: return maxmin<float, GA_OP_MIN>(map, n, x, y, out, ws, s);
+      case GA_F64: return maxmin<double, GA_OP_MIN>(map, n, x, y, out, ws, s);
+      case GA_I32: return maxmin<int32_t, GA_OP_MIN>(map, n, x, y, out, ws, s);
+      case GA_I64: return maxmin<int64_t, GA_OP_MIN>(map, n, x, y, out, ws, s);
+    }
+  }
+  return fail(GA_ERR_INVALID_ARGUMENT, "bad op %d", (int)op);
+}
+
+}  // namespace ga

@@ -1,0 +1,190 @@
+"""GPUArray operations on torch CUDA tensors (§3.2.1).
+
+torch supplies device memory and the stream (plumbing); every operation is
+one call through the C ABI (include/gpuarray.h) into an sm_100a kernel:
+
+    axpbyz(a, x, b, y)    z = a*x + b*y        ElementwiseKernel
+    axpbz(a, x, b)        z = a*x + b          (Listing 1 doubling: a=2, b=-0.0)
+    reduce(op, map, x, y) map-then-reduce       ReductionKernel
+    dot / sum / norm2sq / max / min             instances of reduce
+    scan(x, exclusive)    prefix sum
+
+Reductions return a 0-d tensor that stays on the GPU ("a GPUArray scalar
+still residing on the GPU"); `.item()` is the `.get()`.
+All calls are asynchronous on torch's current stream.
+Errors raise: ValueError for shapes/arguments, TypeError
+for dtypes, RuntimeError for CUDA failures.
+"""
+import builtins
+
+import torch
+
+from . import _abi
+from ._abi import (GA_F32, GA_F64, GA_I32, GA_I64, GA_MAP_ID, GA_MAP_MUL, GA_MAP_SQUARE, GA_OP_MAX, GA_OP_MIN,
+                   GA_OP_SUM, GA_SCAN_EXCLUSIVE, GA_SCAN_INCLUSIVE, check, make_scalar)
+
+SUM, MAX, MIN = GA_OP_SUM, GA_OP_MAX, GA_OP_MIN
+ID, MUL, SQUARE = GA_MAP_ID, GA_MAP_MUL, GA_MAP_SQUARE
+
+_DT = {torch.float32: GA_F32, torch.float64: GA_F64, torch.int32: GA_I32, torch.int64: GA_I64}
+
+
+def ga_dtype(t):
+    try:
+        return _DT[t]
+    except KeyError:
+        raise TypeError(f"unsupported dtype {t}; expected float32/float64/int32/int64") from None
+
+
+def _check_array(name, t):
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if t.dim() != 1:
+        raise ValueError(f"{name} must be 1-D (got shape {tuple(t.shape)})")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    ga_dtype(t.dtype)
+
+
+def _same(x, other, name):
+    _check_array(name, other)
+    if other.shape != x.shape:  # "All these instances are required to have the same length" PAPER.md:457-458
+        raise ValueError(f"{name} has length {other.numel()}, x has {x.numel()}")
+    if other.dtype != x.dtype:
+        raise TypeError(f"{name} has dtype {other.dtype}, x has {x.dtype}")
+    if other.device != x.device:
+        raise ValueError(f"{name} is on {other.device}, x on {x.device}")
+
+
+def _stream(t):
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _ptr(t):
+    return t.data_ptr() if t.numel() else None
+
+
+# --------------------------------------------------------------- workspaces
+# One zero-filled workspace per (kernel family, device, stream); the kernels
+# keep it valid across calls (self-resetting ticket / epoch-tagged scan
+# status), so it is zeroed once at allocation and never again.  Reduce and
+# scan workspaces have different layouts and are never shared.
+_ws = {}
+
+
+def workspace(kind, device, stream, nbytes):
+    key = (kind, device.index, stream)
+    w = _ws.get(key)
+    if w is None or w.numel() < nbytes:
+        size = builtins.max(nbytes, 1 << 16)
+        if w is not None:
+            size = builtins.max(size, 2 * w.numel())
+        w = torch.zeros(size, dtype=torch.uint8, device=device)
+        _ws[key] = w
+    return w
+
+
+# --------------------------------------------------------------- elementwise
+def axpbyz(a, x, b, y, out=None):
+    """z = a*x + b*y in one pass; floats round as RN(RN(a*x)+RN(b*y)) (R1).
+    a and b are converted to x's dtype first (numpy-sized scalars, R2)."""
+    _check_array("x", x)
+    _same(x, y, "y")
+    if out is None:
+        out = torch.empty_like(x)
+    else:
+        _same(x, out, "out")
+    dt = ga_dtype(x.dtype)
+    check(_abi.gpuarray_axpbyz(dt, x.numel(), make_scalar(dt, a), _ptr(x), make_scalar(dt, b), _ptr(y), _ptr(out),
+                               _stream(x)))
+    return out
+
+
+def axpbz(a, x, b, out=None):
+    """z = a*x + b in one pass (RN(RN(a*x)+b))."""
+    _check_array("x", x)
+    if out is None:
+        out = torch.empty_like(x)
+    else:
+        _same(x, out, "out")
+    dt = ga_dtype(x.dtype)
+    check(_abi.gpuarray_axpbz(dt, x.numel(), make_scalar(dt, a), _ptr(x), make_scalar(dt, b), _ptr(out),
+                              _stream(x)))
+    return out
+
+
+# --------------------------------------------------------------- map-reduce
+def reduce(op, map_, x, y=None, out_dtype=None, out=None):
+    """Fold map(x, y) with op from its neutral element; returns a 0-d device
+    tensor of out_dtype (default: x.dtype)."""
+    _check_array("x", x)
+    if map_ == MUL:
+        if y is None:
+            raise ValueError("map MUL needs y")
+        _same(x, y, "y")
+    out_dtype = x.dtype if out_dtype is None else out_dtype
+    if out is None:
+        out = torch.empty((), dtype=out_dtype, device=x.device)
+    elif out.numel() != 1 or out.dtype != out_dtype or out.device != x.device:
+        raise ValueError("out must be a 1-element tensor of out_dtype on x's device")
+    in_dt, out_dt = ga_dtype(x.dtype), ga_dtype(out_dtype)
+    s = _stream(x)
+    nb = _abi.gpuarray_reduce_workspace_bytes(out_dt, x.numel())
+    w = workspace("reduce", x.device, s, nb)
+    check(_abi.gpuarray_reduce(op, map_, in_dt, out_dt, x.numel(), _ptr(x), _ptr(y) if map_ == MUL else None,
+                               out.data_ptr(), w.data_ptr(), w.numel(), s))
+    return out
+
+
+def dot(x, y, out_dtype=None, out=None):
+    """Listing 3b: map x[i]*y[i], reduce a+b, neutral 0."""
+    return reduce(SUM, MUL, x, y, out_dtype=out_dtype, out=out)
+
+
+def sum(x, out_dtype=None, out=None):  # noqa: A001 - numpy-patterned name
+    return reduce(SUM, ID, x, out_dtype=out_dtype, out=out)
+
+
+def norm2sq(x, out_dtype=None, out=None):
+    """Squared 2-norm: map x[i]*x[i], reduce a+b (x is read once)."""
+    return reduce(SUM, SQUARE, x, out_dtype=out_dtype, out=out)
+
+
+def max(x, out=None):  # noqa: A001
+    return reduce(MAX, ID, x, out=out)
+
+
+def min(x, out=None):  # noqa: A001
+    return reduce(MIN, ID, x, out=out)
+
+
+# --------------------------------------------------------------- scan
+def scan(x, exclusive=False, out=None, carry=None):
+    """Prefix sum (int32/int64, wrapping).  `carry` is an optional 1-D device
+    tensor whose elements are all added in front (a sharded scan's offset)."""
+    _check_array("x", x)
+    if out is None:
+        out = torch.empty_like(x)
+    else:
+        _same(x, out, "out")
+    dt = ga_dtype(x.dtype)
+    if carry is not None:
+        _check_array("carry", carry)
+        if carry.dtype != x.dtype or carry.device != x.device:
+            raise TypeError("carry must match x's dtype and device")
+        cptr, ccount = _ptr(carry), carry.numel()
+    else:
+        cptr, ccount = None, 0
+    s = _stream(x)
+    nb = _abi.gpuarray_scan_workspace_bytes(dt, x.numel())
+    w = workspace("scan", x.device, s, nb)
+    kind = GA_SCAN_EXCLUSIVE if exclusive else GA_SCAN_INCLUSIVE
+    check(_abi.gpuarray_scan(SUM, kind, dt, x.numel(), _ptr(x), _ptr(out), cptr, ccount, w.data_ptr(), w.numel(), s))
+    return out
+
+
+def launch_count():
+    """Kernels launched by libgpuarray.so in this process."""
+    return _abi.gpuarray_launch_count()

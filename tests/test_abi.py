@@ -1,0 +1,105 @@
+"""CPU-side checks of the boundary: the C-ABI library loads, exports every
+symbol include/gpuarray.h declares, and validates arguments synchronously
+(no kernel is launched for invalid calls, so these run without a GPU)."""
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "gpuarray.h")).read()
+    return sorted(set(re.findall(r"\b(gpuarray_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def abi():
+    from paper_1304_5553_b200 import build
+    build.build()
+    from paper_1304_5553_b200 import _abi
+    return _abi
+
+
+def test_exports_every_declared_symbol(abi):
+    declared = header_symbols()
+    assert len(declared) == 10
+    assert sorted(abi.EXPORTS) == declared
+    for name in declared:
+        assert hasattr(abi.LIB, name), name
+
+
+def test_nm_shows_c_linkage(abi):
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", abi.LIB_PATH], capture_output=True, text=True).stdout
+    for name in header_symbols():
+        assert re.search(rf"\bT {name}$", out, re.M), name
+
+
+def test_version_and_strings(abi):
+    assert abi.gpuarray_abi_version() == 1
+    assert abi.gpuarray_status_string(abi.GA_OK) == "GA_OK"
+    assert abi.gpuarray_status_string(abi.GA_ERR_CUDA) == "GA_ERR_CUDA"
+    assert abi.gpuarray_status_string(99) == "GA_ERR_UNKNOWN"
+
+
+def test_workspace_sizes(abi):
+    assert abi.gpuarray_reduce_workspace_bytes(abi.GA_F32, 1 << 30) >= 128 + 8 * 1184
+    a = abi.gpuarray_scan_workspace_bytes(abi.GA_I32, 1 << 30)
+    assert a == 256 + 8 * ((1 << 30) // 4096)
+    b = abi.gpuarray_scan_workspace_bytes(abi.GA_I64, 1 << 20)
+    assert b >= 256 + 20 * ((1 << 20) // 2048)
+    assert abi.gpuarray_scan_workspace_bytes(abi.GA_F32, 100) == 0   # not instantiated
+
+
+def test_argument_validation_is_synchronous(abi):
+    f32 = abi.make_scalar(abi.GA_F32, 1.0)
+    f64 = abi.make_scalar(abi.GA_F64, 1.0)
+    E = abi.GA_ERR_INVALID_ARGUMENT
+    assert abi.gpuarray_axpbyz(abi.GA_F32, -1, f32, None, f32, None, None, None) == E
+    assert abi.gpuarray_axpbyz(abi.GA_F32, 0, f32, None, f32, None, None, None) == abi.GA_OK  # no-op
+    assert abi.gpuarray_axpbyz(abi.GA_F32, 4, f32, 4096, f64, 8192, 12288, None) == E        # scalar dtype
+    assert "scalar dtype" in abi.gpuarray_last_error()
+    assert abi.gpuarray_axpbyz(abi.GA_F32, 4, f32, None, f32, 8192, 12288, None) == E         # NULL x
+    assert abi.gpuarray_axpbyz(abi.GA_F32, 16, f32, 4096, f32, 8192, 4100, None) == E         # partial overlap
+    assert abi.gpuarray_axpbyz(7, 4, f32, 4096, f32, 8192, 12288, None) == E                  # bad dtype
+    assert abi.gpuarray_axpbz(abi.GA_F32, 4, f32, 4096, f64, 12288, None) == E
+    ws = abi.gpuarray_reduce_workspace_bytes(abi.GA_F32, 4)
+    R = abi.gpuarray_reduce
+    assert R(5, 0, 0, 0, 4, 4096, None, 64, 128, ws, None) == E                                # bad op
+    assert R(0, 5, 0, 0, 4, 4096, None, 64, 128, ws, None) == E                                # bad map
+    assert R(0, abi.GA_MAP_MUL, 0, 0, 4, 4096, None, 64, 128, ws, None) == E                   # MUL without y
+    assert R(0, 0, 0, 0, 4, 4096, None, None, 128, ws, None) == E                              # no out
+    assert R(0, 0, 0, 0, 4, 4096, None, 64, 128, ws - 1, None) == abi.GA_ERR_WORKSPACE
+    assert R(0, 0, 0, 0, 4, 4096, None, 64, None, ws, None) == abi.GA_ERR_WORKSPACE
+    S = abi.gpuarray_scan
+    sw = abi.gpuarray_scan_workspace_bytes(abi.GA_I32, 100)
+    assert S(abi.GA_OP_MAX, 0, abi.GA_I32, 100, 4096, 8192, None, 0, 64, sw, None) == abi.GA_ERR_UNSUPPORTED
+    assert S(0, 0, abi.GA_F32, 100, 4096, 8192, None, 0, 64, sw, None) == abi.GA_ERR_UNSUPPORTED
+    assert S(0, 3, abi.GA_I32, 100, 4096, 8192, None, 0, 64, sw, None) == E                   # bad kind
+    assert S(0, 0, abi.GA_I32, 100, 4096, 8192, None, 2, 64, sw, None) == E                   # carry NULL
+    assert S(0, 0, abi.GA_I32, 100, 4096, 4100, None, 0, 64, sw, None) == E                   # partial overlap
+    assert S(0, 0, abi.GA_I32, 100, 4096, 8192, None, 0, 64, sw - 1, None) == abi.GA_ERR_WORKSPACE
+    assert S(0, 0, abi.GA_I32, 0, None, None, None, 0, None, 0, None) == abi.GA_OK           # n == 0 no-op
+
+
+def test_python_error_mapping(abi):
+    with pytest.raises(ValueError):
+        abi.check(abi.GA_ERR_INVALID_ARGUMENT)
+    with pytest.raises(TypeError):
+        abi.check(abi.GA_ERR_UNSUPPORTED)
+    with pytest.raises(RuntimeError):
+        abi.check(abi.GA_ERR_CUDA)
+
+
+def test_scalar_marshalling(abi):
+    import struct
+    s = abi.make_scalar(abi.GA_F32, 5.7)
+    assert struct.unpack("<f", struct.pack("<Q", s.bits)[:4])[0] == struct.unpack("<f", struct.pack("<f", 5.7))[0]
+    s = abi.make_scalar(abi.GA_I32, -1)
+    assert s.bits == 0xFFFFFFFF
+    s = abi.make_scalar(abi.GA_I64, -2)
+    assert s.bits == (1 << 64) - 2
+    import ctypes
+    assert ctypes.sizeof(abi.ga_scalar_t) == 16

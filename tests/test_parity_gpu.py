@@ -1,0 +1,338 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element on the same seeded inputs.  Bars:
+  - elementwise: bit-exact (<= 1 ulp is the stated bound; 0 is the target)
+  - integer reductions / scans, float max/min: bit-exact
+  - float SUM (sum/dot/norm2): |gpu - oracle| <= max(tol_rel*|oracle|, n*u*sum|t_i|),
+    tol_rel = 1e-5 (fp32 accumulation) / 1e-12 (fp64), u = 2^-24 / 2^-53,
+    and the flat tol_rel*|oracle| clause is ALSO asserted alone (R10).
+Sizes span several tiles plus ragged tails; offsets make unaligned views."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+
+if torch.cuda.is_available():
+    import paper_1304_5553_b200 as ga
+    from paper_1304_5553_b200 import gpuarray as G
+
+DEV = "cuda:0"
+SIZES = [1, 2, 3, 7, 31, 32, 33, 255, 256, 257, 4095, 4096, 4097, 8191, 8193, 65536 + 13,
+         (1 << 20) - (1 << 18) + 5]
+NPT = {np.float32: torch.float32, np.float64: torch.float64, np.int32: torch.int32, np.int64: torch.int64}
+
+
+def to_dev(a, offset=0):
+    """Copy numpy `a` to the GPU as a contiguous view starting `offset` elements
+    into a fresh allocation (offset > 0 makes the view unaligned)."""
+    buf = torch.empty(a.size + offset, dtype=NPT[a.dtype.type], device=DEV)
+    v = buf[offset:]
+    v.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+    return v
+
+
+def host_data(dt, n, seed, signed=False, ints=(-1000, 1000)):
+    if dt == np.float32:
+        return synth.host_fill(synth.F32_S11 if signed else synth.F32_U01, seed, n)
+    if dt == np.float64:
+        return synth.host_fill(synth.F64_S11 if signed else synth.F64_U01, seed, n)
+    if dt == np.int32:
+        return synth.host_fill(synth.I32_RANGE, seed, n, lo=ints[0], hi=ints[1])
+    return synth.host_fill(synth.I64_RANGE, seed, n, lo=ints[0], hi=ints[1])
+
+
+def bits(a):
+    a = np.asarray(a)
+    return a.view({4: np.uint32, 8: np.uint64}[a.dtype.itemsize])
+
+
+def assert_bit_exact(got, ref):
+    assert got.dtype == ref.dtype and got.shape == ref.shape
+    if got.dtype.kind == "f":
+        nan = np.isnan(got) & np.isnan(ref)
+        bad = (bits(got) != bits(ref)) & ~nan
+    else:
+        bad = got != ref
+    if bad.any():
+        i = int(np.argmax(bad))
+        raise AssertionError(f"{int(bad.sum())} mismatches; first at {i}: gpu={got[i]!r} oracle={ref[i]!r}")
+
+
+# ------------------------------------------------------------------ elementwise
+@pytest.mark.parametrize("dt", [np.float32, np.float64, np.int32, np.int64])
+@pytest.mark.parametrize("n", SIZES)
+def test_axpbyz_bit_exact(dt, n):
+    x = host_data(dt, n, 1, signed=True)
+    y = host_data(dt, n, 2, signed=True)
+    a, b = (5.0, -6.0) if np.dtype(dt).kind == "f" else (123457, -98765)
+    z = ga.axpbyz(a, to_dev(x), b, to_dev(y)).cpu().numpy()
+    assert_bit_exact(z, oracle.axpbyz(dt(a), x, dt(b), y))
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("offs", [(1, 1, 1), (3, 3, 3), (7, 7, 7), (1, 2, 3), (0, 5, 0), (2, 0, 0)])
+def test_axpbyz_unaligned_views(dt, offs):
+    n = 10007
+    x = host_data(dt, n, 1)
+    y = host_data(dt, n, 2)
+    out = torch.empty(n + offs[2], dtype=NPT[dt], device=DEV)[offs[2]:]
+    G.axpbyz(5.7, to_dev(x, offs[0]), -1.25, to_dev(y, offs[1]), out=out)
+    assert_bit_exact(out.cpu().numpy(), oracle.axpbyz(dt(5.7), x, dt(-1.25), y))
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.int64])
+def test_axpbyz_inplace(dt):
+    n = 70001
+    x = host_data(dt, n, 1)
+    y = host_data(dt, n, 2)
+    xd, yd = to_dev(x), to_dev(y)
+    ref = oracle.axpbyz(dt(3), x, dt(2), y)
+    G.axpbyz(3, xd, 2, yd, out=xd)      # z == x
+    assert_bit_exact(xd.cpu().numpy(), ref)
+    xd = to_dev(x)
+    G.axpbyz(3, xd, 2, yd, out=yd)      # z == y
+    assert_bit_exact(yd.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64, np.int32, np.int64])
+@pytest.mark.parametrize("n", [1, 9, 4097, 65536 + 13])
+def test_axpbz_bit_exact(dt, n):
+    x = host_data(dt, n, 3, signed=True)
+    a, b = (5.7, -0.3) if np.dtype(dt).kind == "f" else (-77, 12345)
+    z = ga.axpbz(a, to_dev(x, 1), b).cpu().numpy()
+    assert_bit_exact(z, oracle.axpbz(dt(a), x, dt(b)))
+
+
+def test_listing1_doubling(golden):
+    """Listing 1/2: 4x4 fp32 times two, incl. -0.0."""
+    g = golden("listing1_doubling.json")
+    x = np.array(g["input"], np.float32).ravel()
+    z = ga.axpbz(2.0, to_dev(x), -0.0).cpu().numpy()
+    assert_bit_exact(z, np.array(g["output"], np.float32).ravel())
+
+
+def test_listing4_vector_add(golden):
+    g = golden("listing4_vector_add.json")
+    x, y, zr = (np.array(g[k], np.float32) for k in ("x", "y", "z"))
+    assert_bit_exact(ga.axpbyz(1.0, to_dev(x), 1.0, to_dev(y)).cpu().numpy(), zr)
+
+
+def test_elementwise_special_values():
+    x = np.array([np.inf, -np.inf, np.nan, 0.0, -0.0, 1e-45, 3.4e38, -3.4e38, 1.0], np.float32)
+    y = np.array([1.0, np.inf, 2.0, -0.0, -0.0, 1e-45, 3.4e38, 3.4e38, np.nan], np.float32)
+    z = ga.axpbyz(2.0, to_dev(x), 3.0, to_dev(y)).cpu().numpy()
+    with np.errstate(all="ignore"):
+        assert_bit_exact(z, oracle.axpbyz(np.float32(2), x, np.float32(3), y))
+
+
+def test_elementwise_empty_and_errors():
+    e = torch.empty(0, device=DEV)
+    assert ga.axpbyz(1.0, e, 1.0, e).numel() == 0
+    with pytest.raises(ValueError):
+        ga.axpbyz(1.0, torch.ones(3, device=DEV), 1.0, torch.ones(4, device=DEV))
+    with pytest.raises(TypeError):
+        ga.axpbyz(1.0, torch.ones(3, device=DEV), 1.0, torch.ones(3, device=DEV, dtype=torch.float64))
+    with pytest.raises(ValueError):
+        ga.axpbyz(1.0, torch.ones(3), 1.0, torch.ones(3))  # CPU tensors: no CPU path
+    buf = torch.ones(10, device=DEV)
+    with pytest.raises(ValueError):  # partial overlap of z with x
+        G.axpbyz(1.0, buf[0:8], 1.0, torch.ones(8, device=DEV), out=buf[1:9])
+
+
+# ------------------------------------------------------------------ reductions
+def float_tol(dt, n, ref, sumabs):
+    rel, u = (1e-5, 2.0 ** -24) if dt == np.float32 else (1e-12, 2.0 ** -53)
+    return max(rel * abs(ref), n * u * sumabs), rel * abs(ref)
+
+
+@pytest.mark.parametrize("dt,odt", [(np.float32, np.float32), (np.float32, np.float64), (np.float64, np.float64)])
+@pytest.mark.parametrize("mp", [oracle.MAP_ID, oracle.MAP_MUL, oracle.MAP_SQUARE])
+@pytest.mark.parametrize("n", [1, 2, 7, 33, 257, 4097, 65536 + 13, (1 << 20) - (1 << 18) + 5, 3_000_017])
+@pytest.mark.parametrize("signed", [False, True])
+def test_float_sum_within_tolerance(dt, odt, mp, n, signed):
+    x = host_data(dt, n, 1, signed=signed)
+    y = host_data(dt, n, 2, signed=signed)
+    got = float(G.reduce(G.SUM, mp, to_dev(x), to_dev(y) if mp == G.MUL else None, out_dtype=NPT[odt]).item())
+    ref, sa = oracle.reduce(oracle.SUM, mp, x, y, return_sumabs=True)
+    tol, flat = float_tol(odt, n, ref, sa)
+    assert abs(got - ref) <= tol
+    if not signed:
+        # no cancellation: the flat relative clause must hold on its own (R10)
+        assert abs(got - ref) <= flat
+
+
+@pytest.mark.parametrize("in_dt,out_dt", [(np.int32, np.int32), (np.int32, np.int64), (np.int64, np.int64)])
+@pytest.mark.parametrize("mp", [oracle.MAP_ID, oracle.MAP_MUL, oracle.MAP_SQUARE])
+@pytest.mark.parametrize("n", [0, 1, 2, 255, 256, 257, 4097, 65536, 1_000_003])
+def test_int_sum_bit_exact(in_dt, out_dt, mp, n):
+    info = np.iinfo(in_dt)
+    rng = np.random.default_rng(n)
+    x = rng.integers(info.min, info.max, size=n, dtype=in_dt, endpoint=True)
+    y = rng.integers(info.min, info.max, size=n, dtype=in_dt, endpoint=True)
+    got = int(G.reduce(G.SUM, mp, to_dev(x, 1), to_dev(y, 3) if mp == G.MUL else None, out_dtype=NPT[out_dt]).item())
+    assert got == oracle.reduce(oracle.SUM, mp, x, y, out_dtype=out_dt)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64, np.int32, np.int64])
+@pytest.mark.parametrize("op", [oracle.MAX, oracle.MIN])
+@pytest.mark.parametrize("mp", [oracle.MAP_ID, oracle.MAP_MUL, oracle.MAP_SQUARE])
+@pytest.mark.parametrize("n", [0, 1, 255, 256, 257, 4097, 100_000, 1_000_003])
+def test_maxmin_bit_exact(dt, op, mp, n):
+    if np.dtype(dt).kind == "f":
+        x = host_data(dt, n, 4, signed=True)
+        y = host_data(dt, n, 5, signed=True)
+    else:
+        info = np.iinfo(dt)
+        rng = np.random.default_rng(n + 7)
+        x = rng.integers(info.min, info.max, size=n, dtype=dt, endpoint=True)
+        y = rng.integers(info.min, info.max, size=n, dtype=dt, endpoint=True)
+    got = G.reduce(op, mp, to_dev(x), to_dev(y, 2) if mp == G.MUL else None).cpu().numpy()
+    ref = oracle.reduce(op, mp, x, y)
+    if np.dtype(dt).kind == "f":
+        assert got == ref or (got == 0 and ref == 0)  # sign of a zero extreme: unpinned (R7)
+    else:
+        assert int(got) == ref
+
+
+def test_maxmin_planted_and_nan():
+    n = 1 << 20
+    for pos in (0, n - 1, 123457):
+        x = synth.host_fill(synth.F32_S11, 4, n)
+        x[pos] = 7.0
+        assert float(ga.max(to_dev(x)).item()) == 7.0
+        x[pos] = -7.0
+        assert float(ga.min(to_dev(x)).item()) == -7.0
+    x = np.array([1, np.nan, 3, -2], np.float32)
+    assert float(ga.max(to_dev(x)).item()) == 3.0
+    assert float(ga.min(to_dev(x)).item()) == -2.0
+    allnan = np.full(1000, np.nan, np.float32)
+    assert float(ga.max(to_dev(allnan)).item()) == oracle.reduce(oracle.MAX, oracle.MAP_ID, allnan) == -np.inf
+
+
+def test_reduce_spec_examples(golden):
+    g = golden("dot_spec_example.json")
+    assert float(ga.dot(to_dev(np.array(g["x"], np.float32)), to_dev(np.array(g["y"], np.float32))).item()) == g["dot"]
+    g = golden("sum_1_to_8.json")
+    assert int(ga.sum(to_dev(np.array(g["input"], np.int32))).item()) == g["sum"]
+    g = golden("min_neutral_spec.json")
+    assert int(ga.min(torch.empty(0, dtype=torch.int32, device=DEV)).item()) == g["empty_min"]
+    x = to_dev(np.array(g["input"], np.int32))
+    assert int(ga.min(x).item()) == g["min"] and int(ga.max(x).item()) == g["max"]
+
+
+def test_reduce_closed_forms():
+    n = 1 << 24
+    ramp = torch.arange(1, n + 1, dtype=torch.float64, device=DEV)
+    assert float(ga.sum(ramp).item()) == n * (n + 1) / 2
+    twos = torch.full((1 << 20,), 2.0, device=DEV)
+    r0 = torch.arange(0, 1 << 20, dtype=torch.float32, device=DEV)
+    m = 1 << 20
+    assert float(ga.dot(twos, r0).item()) == pytest.approx(m * (m - 1), rel=1e-6)
+    assert float(ga.norm2sq(torch.ones(m, device=DEV)).item()) == m
+
+
+def test_reduce_empty_is_neutral():
+    e32 = torch.empty(0, device=DEV)
+    assert float(ga.sum(e32).item()) == 0.0
+    assert float(ga.max(e32).item()) == -np.inf
+    assert float(ga.min(e32).item()) == np.inf
+    assert int(ga.max(torch.empty(0, dtype=torch.int64, device=DEV)).item()) == -(1 << 63)
+
+
+def test_reduce_deterministic_and_reusable():
+    n = (1 << 24) + 11
+    x = synth.device_fill(synth.F32_S11, 1, n, device=DEV)
+    y = synth.device_fill(synth.F32_S11, 2, n, device=DEV)
+    vals = {float(ga.dot(x, y).item()) for _ in range(5)}
+    assert len(vals) == 1
+    # different sizes back to back reuse the same workspace (ticket self-resets)
+    for m in (5, 1 << 20, 3, n):
+        xs = x[:m]
+        xh = synth.host_fill(synth.F32_S11, 1, m)
+        ref, sa = oracle.reduce(oracle.SUM, oracle.MAP_ID, xh, None, return_sumabs=True)
+        assert abs(float(ga.sum(xs).item()) - ref) <= float_tol(np.float32, m, ref, sa)[0]
+
+
+def test_reduce_unsupported_combos():
+    x = torch.ones(10, device=DEV)
+    with pytest.raises(TypeError):
+        G.reduce(G.MAX, G.ID, x, out_dtype=torch.float64)
+    with pytest.raises(TypeError):
+        G.reduce(G.SUM, G.ID, x, out_dtype=torch.int32)
+    with pytest.raises(ValueError):
+        G.reduce(G.SUM, G.MUL, x)
+
+
+# ------------------------------------------------------------------ scan
+SCAN_SIZES = [1, 2, 31, 32, 33, 2047, 2048, 2049, 4095, 4096, 4097, 3 * 4096 + 1, 65536 + 13, 1_000_003,
+              (1 << 20) - (1 << 18) + 5]
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.int64])
+@pytest.mark.parametrize("exclusive", [False, True])
+@pytest.mark.parametrize("n", SCAN_SIZES)
+def test_scan_bit_exact(dt, exclusive, n):
+    x = synth.host_fill(synth.I32_RANGE if dt == np.int32 else synth.I64_RANGE, 3, n, lo=-(1 << 20), hi=1 << 20)
+    got = ga.scan(to_dev(x), exclusive=exclusive).cpu().numpy()
+    assert_bit_exact(got, oracle.scan(oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE, x))
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.int64])
+def test_scan_wraps_unaligned_inplace_carry(dt):
+    info = np.iinfo(dt)
+    rng = np.random.default_rng(5)
+    n = 300_007
+    x = rng.integers(info.min, info.max, size=n, dtype=dt, endpoint=True)   # wraps constantly
+    for offs in (0, 1, 5):
+        got = ga.scan(to_dev(x, offs)).cpu().numpy()
+        assert_bit_exact(got, oracle.scan(oracle.INCLUSIVE, x))
+    xd = to_dev(x)
+    G.scan(xd, exclusive=True, out=xd)  # in place
+    assert_bit_exact(xd.cpu().numpy(), oracle.scan(oracle.EXCLUSIVE, x))
+    carry = np.array([info.max, 12345, -7], dt)
+    with np.errstate(over="ignore"):
+        c = dt(np.add.reduce(carry, dtype=dt))
+    for ex in (False, True):
+        got = G.scan(to_dev(x), exclusive=ex, carry=to_dev(carry)).cpu().numpy()
+        assert_bit_exact(got, oracle.scan(oracle.EXCLUSIVE if ex else oracle.INCLUSIVE, x, carry=c))
+
+
+def test_scan_spec_example_and_closed_forms(golden):
+    g = golden("scan_spec_example.json")
+    x = to_dev(np.array(g["input"], np.int32))
+    assert ga.scan(x).cpu().tolist() == g["inclusive"]
+    assert ga.scan(x, exclusive=True).cpu().tolist() == g["exclusive"]
+    n = 5_000_011
+    ones = torch.ones(n, dtype=torch.int32, device=DEV)
+    assert torch.equal(ga.scan(ones), torch.arange(1, n + 1, dtype=torch.int32, device=DEV))
+    assert torch.equal(ga.scan(ones, exclusive=True), torch.arange(0, n, dtype=torch.int32, device=DEV))
+
+
+def test_scan_reduce_consistency_and_reuse():
+    """Last inclusive element == reduce SUM; many calls of
+    different sizes on one workspace (epoch tags, self-resetting counter)."""
+    for n in (100_000, 3, 4096 * 50 + 7, 1, 100_000, 2_000_000):
+        x = synth.device_fill(synth.I32_RANGE, 3, n, lo=0, hi=9, device=DEV)
+        s = ga.scan(x)
+        assert int(s[-1].item()) == int(ga.sum(x).item())
+        xh = synth.host_fill(synth.I32_RANGE, 3, n, lo=0, hi=9)
+        assert_bit_exact(s.cpu().numpy(), oracle.scan(oracle.INCLUSIVE, xh))
+
+
+def test_scan_empty_and_errors():
+    e = torch.empty(0, dtype=torch.int32, device=DEV)
+    assert ga.scan(e).numel() == 0
+    with pytest.raises(TypeError):
+        ga.scan(torch.ones(4, device=DEV))  # fp32 scan not instantiated
+
+
+def test_launch_accounting():
+    x = torch.ones(1000, device=DEV)
+    c0 = ga.launch_count()
+    ga.axpbyz(1.0, x, 1.0, x)
+    ga.sum(x)
+    ga.scan(torch.ones(1000, dtype=torch.int32, device=DEV))
+    assert ga.launch_count() - c0 == 3
