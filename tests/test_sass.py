@@ -1,0 +1,77 @@
+"""Static evidence from the compiled sm_100a library (no GPU needed):
+  - the elementwise kernels keep the R1 rounding sequence: FMUL/FADD
+    (DMUL/DADD), never FFMA/DFMA;
+  - the hot loops move 256-bit vectors (LDG.E...256 / STG.E...256) and the
+    scan moves 128-bit rows;
+  - no kernel spills to local memory."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(ROOT, "paper_1304_5553_b200", "libgpuarray.so")
+
+
+@pytest.fixture(scope="module")
+def sass():
+    from paper_1304_5553_b200 import build
+    build.build()
+    out = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
+    funcs = {}
+    cur = None
+    for line in out.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            cur = m.group(1)
+            funcs[cur] = []
+        elif cur:
+            funcs[cur].append(line)
+    return {k: "\n".join(v) for k, v in funcs.items()}
+
+
+def demangled_kind(name):
+    return subprocess.run(["c++filt", name], capture_output=True, text=True).stdout.strip()
+
+
+def test_arch_is_sm100a():
+    out = subprocess.run(["cuobjdump", "-lelf", LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_elementwise_float_has_no_fma(sass):
+    n = 0
+    for name, body in sass.items():
+        d = demangled_kind(name)
+        if "ew_vec_kernel<float" in d or "ew_scalar_kernel<float" in d:
+            assert "FFMA" not in body, d
+            assert "FMUL" in body and "FADD" in body, d
+            n += 1
+        if "ew_vec_kernel<double" in d or "ew_scalar_kernel<double" in d:
+            assert "DFMA" not in body, d
+            assert "DMUL" in body and "DADD" in body, d
+            n += 1
+    assert n >= 8
+
+
+def test_vector_widths(sass):
+    seen = {"ew": False, "red": False, "scan": False}
+    for name, body in sass.items():
+        d = demangled_kind(name)
+        if "ew_vec_kernel" in d:
+            assert re.search(r"LDG\.E\S*\.256", body) and re.search(r"STG\.E\S*\.256", body), d
+            seen["ew"] = True
+        if "reduce_kernel" in d:
+            assert re.search(r"LDG\.E\S*\.256", body), d
+            seen["red"] = True
+        if "scan_l2_kernel" in d:
+            assert re.search(r"LDG\.E\S*\.128", body) and re.search(r"STG\.E\S*\.128", body), d
+            seen["scan"] = True
+    assert all(seen.values()), seen
+
+
+def test_no_local_memory_spills():
+    out = subprocess.run(["cuobjdump", "-res-usage", LIB], capture_output=True, text=True).stdout
+    locs = [int(x) for x in re.findall(r"LOCAL:(\d+)", out)]
+    assert locs and max(locs) == 0

@@ -1,0 +1,108 @@
+"""Summarise ncu captures into profiles/ (committed evidence).
+
+    python tools/summarize_ncu.py <round-tag> <full.ncu-rep> [launches.csv]
+
+Writes profiles/<tag>_kernels.md (per-kernel metrics of the --set full
+capture), profiles/<tag>_launches.md (share of each kernel in the launch
+list of a bench run) and updates profiles/ncu_traffic.json (DRAM bytes per
+launch of each hot-path kernel, read by bench.py's roofline.traffic)."""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PROF = os.path.join(ROOT, "profiles")
+
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "dram_read"),
+    ("dram__bytes_write.sum", "dram_write"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_%peak"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy_%"),
+    ("launch__registers_per_thread", "regs"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+    ("lts__t_sector_hit_rate.pct", "l2_hit_%"),
+]
+
+
+def op_of(name):
+    if "ew_vec_kernel" in name:
+        return "axpbyz" if ", true" in name or "1, 2" in name else "axpbz"
+    if "reduce_kernel" in name:
+        mp = name.split("reduce_kernel<")[1].split(">")[0].split(",")
+        m = mp[3].strip()
+        return {"0": "sum", "1": "dot", "2": "norm2"}.get(m, "reduce")
+    if "scan" in name:
+        return "scan"
+    return name[:40]
+
+
+def raw_rows(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    return hdr, units, rows[2:]
+
+
+def to_bytes(v, unit):
+    v = float(v)
+    return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
+
+
+def main():
+    tag, rep = sys.argv[1], sys.argv[2]
+    launches = sys.argv[3] if len(sys.argv) > 3 else None
+    os.makedirs(PROF, exist_ok=True)
+    hdr, units, rows = raw_rows(rep)
+    idx = {k: hdr.index(k) for k, _ in KEYS if k in hdr}
+    lines = [f"# {tag}: ncu --set full --clock-control none (one launch per kernel, n = 2^28)", "",
+             "Source: `" + os.path.basename(rep) + "` (gpurun_out/, not committed). Durations are ncu's "
+             "(serialised, cold-ish L2); compare shares, not absolutes, with bench.py.", "",
+             "| op | kernel | " + " | ".join(n for _, n in KEYS) + " | DRAM GB/s |", "|" + "---|" * (len(KEYS) + 3)]
+    traffic_path = os.path.join(PROF, "ncu_traffic.json")
+    traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    for r in rows:
+        name = r[hdr.index("Kernel Name")]
+        op = op_of(name)
+        vals = []
+        for k, _ in KEYS:
+            vals.append(r[idx[k]] + " " + units[idx[k]] if k in idx else "-")
+        rd = to_bytes(r[idx["dram__bytes_read.sum"]], units[idx["dram__bytes_read.sum"]])
+        wr = to_bytes(r[idx["dram__bytes_write.sum"]], units[idx["dram__bytes_write.sum"]])
+        dur = float(r[idx["gpu__time_duration.sum"]]) * {"ns": 1e-9, "us": 1e-6, "ms": 1e-3}[units[idx["gpu__time_duration.sum"]]]
+        lines.append(f"| {op} | `{name[:70]}` | " + " | ".join(vals) + f" | {(rd + wr) / dur / 1e9:.0f} |")
+        traffic[f"{op}@2^28"] = int(rd + wr)
+    open(os.path.join(PROF, f"{tag}_kernels.md"), "w").write("\n".join(lines) + "\n")
+    json.dump(traffic, open(traffic_path, "w"), indent=1, sort_keys=True)
+    if launches:
+        text = open(launches).read()
+        start = text.find('"ID"')
+        rows = list(csv.reader(io.StringIO(text[start:])))
+        h = rows[0]
+        ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+        tot = defaultdict(float)
+        cnt = defaultdict(int)
+        for r in rows[1:]:
+            if len(r) <= vi:
+                continue
+            v = float(r[vi].replace(",", "")) * {"ns": 1e-3, "us": 1, "ms": 1e3}.get(r[ui], 1)
+            op = op_of(r[ki])
+            tot[op] += v
+            cnt[op] += 1
+        all_t = sum(tot.values())
+        out = [f"# {tag}: launch list of `bench.py --steps 3 --warmup 3` under "
+               "`ncu --metrics gpu__time_duration.sum --clock-control none`", "",
+               "Cold-cache, serialised per-launch times: the SHARE column is what must agree with bench.py's "
+               "per-op split (ops.*.ms).", "", "| kernel (op) | launches | total us | mean us | share |", "|---|---|---|---|---|"]
+        for op in sorted(tot, key=lambda o: -tot[o]):
+            out.append(f"| {op} | {cnt[op]} | {tot[op]:.1f} | {tot[op] / cnt[op]:.1f} | {tot[op] / all_t * 100:.1f}% |")
+        open(os.path.join(PROF, f"{tag}_launches.md"), "w").write("\n".join(out) + "\n")
+
+
+if __name__ == "__main__":
+    main()
