@@ -119,55 +119,74 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle leg
-def oracle_sample(log2n_sample, threads_note="1 (single-threaded plain C oracle)"):
-    """Time the oracle (as it stands) on a bounded sample of the workload:
-    the same five ops on 2^log2n_sample elements regenerated by the synth host
-    twin.  Returns (GB/s, seconds, sample description)."""
-    import numpy as np
+class OracleStep:
+    """The oracle (as it stands, single-threaded plain C) on a bounded sample
+    of the workload: the same five ops on 2^log2m elements regenerated once
+    by the synth host twin.  Only the compute is timed."""
 
-    import oracle
-    import synth
-    m = 1 << log2n_sample
-    x = synth.host_fill(synth.F32_U01, synth.SEED_X, m)
-    y = synth.host_fill(synth.F32_U01, synth.SEED_Y, m)
-    k = synth.host_fill(synth.I32_RANGE, synth.SEED_INT, m, lo=0, hi=9)
-    t0 = time.perf_counter()
-    oracle.axpbyz(np.float32(A), x, np.float32(B), y)
-    oracle.reduce(oracle.SUM, oracle.MAP_MUL, x, y)
-    oracle.reduce(oracle.SUM, oracle.MAP_ID, x)
-    oracle.reduce(oracle.SUM, oracle.MAP_SQUARE, x)
-    oracle.scan(oracle.EXCLUSIVE, k)
-    dt = time.perf_counter() - t0
-    nbytes = m * sum(OP_BYTES.values())
-    desc = (f"2^{log2n_sample} elements per op (axpbyz/dot/sum/norm2 fp32 + exclusive scan int32), "
-            f"inputs regenerated by the synth host twin; oracle compute only; threads: {threads_note}")
-    return nbytes / dt / 1e9, dt, desc
+    def __init__(self, log2m):
+        import oracle
+        import synth
+        self.oracle = oracle
+        self.m = 1 << log2m
+        self.log2m = log2m
+        self.x = synth.host_fill(synth.F32_U01, synth.SEED_X, self.m)
+        self.y = synth.host_fill(synth.F32_U01, synth.SEED_Y, self.m)
+        self.k = synth.host_fill(synth.I32_RANGE, synth.SEED_INT, self.m, lo=0, hi=9)
+
+    def __call__(self):
+        import numpy as np
+        o = self.oracle
+        t0 = time.perf_counter()
+        o.axpbyz(np.float32(A), self.x, np.float32(B), self.y)
+        o.reduce(o.SUM, o.MAP_MUL, self.x, self.y)
+        o.reduce(o.SUM, o.MAP_ID, self.x)
+        o.reduce(o.SUM, o.MAP_SQUARE, self.x)
+        o.scan(o.EXCLUSIVE, self.k)
+        return time.perf_counter() - t0
+
+    @property
+    def bytes(self):
+        return self.m * sum(OP_BYTES.values())
+
+    def describe(self):
+        return (f"2^{self.log2m} elements per op (axpbyz/dot/sum/norm2 fp32 + exclusive scan int32) of the same "
+                f"synthetic streams, regenerated once by the synth host twin; oracle compute only; "
+                f"1 thread (plain single-threaded C, -O2 -ffp-contract=off)")
+
+
+def oracle_sample(log2m, reps=3):
+    step = OracleStep(log2m)
+    step()
+    secs = min(step() for _ in range(reps))
+    return step.bytes / secs / 1e9, secs, step.describe()
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the CPU oracle on host cores (rank 0 only)."""
+    """--impl reference: the CPU oracle on the host cores (rank 0 only; the
+    paper ships no code, so the oracle is the reference arm)."""
     if rank != 0:
         return
-    log2s = min(args.log2n, 24)
-    for _ in range(max(args.warmup, 0) and 1):
-        oracle_sample(log2s)
-    rates, times = [], []
-    for _ in range(max(args.steps, 1) if args.steps <= 3 else 3):
-        r, t, desc = oracle_sample(log2s)
-        rates.append(r)
-        times.append(t)
-    gbs = statistics.median(rates)
-    ms_per_step_full = (N_PER_GPU if args.log2n == LOG2_N else (1 << args.log2n)) * sum(OP_BYTES.values()) / (gbs * 1e9) * 1e3
+    step = OracleStep(min(args.log2n, 24))
+    for _ in range(max(args.warmup, 1)):
+        step()
+    times = [step() for _ in range(max(args.steps, 1))]
+    total = sum(times)
+    gbs = step.bytes * len(times) / total / 1e9
+    n_full = 1 << args.log2n
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world,
-        "steps": len(rates), "warmup": args.warmup, "ms_per_step": round(ms_per_step_full, 3),
+        "steps": len(times), "warmup": max(args.warmup, 1), "ms_per_step": round(total / len(times) * 1e3, 3),
+        "ms_per_full_step_extrapolated": round(n_full * sum(OP_BYTES.values()) / (gbs * 1e9) * 1e3, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+i32", "data": "synthetic",
         "config": {"workload": f"configs[1]-sized step per GPU: axpbyz+dot+sum+norm2 fp32 and exclusive scan "
-                               f"int32 on n=2^{args.log2n}; oracle sample 2^{log2s}", "parallelism": "cpu"},
-        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc},
+                               f"int32 on n=2^{args.log2n}; each reference step is a 2^{step.log2m}-element sample",
+                   "parallelism": "cpu, 1 thread"},
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": step.describe()},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "no reference code exists (the paper ships none); the reference arm is the CPU oracle, "
-                "timed on a bounded sample, ms_per_step extrapolated to the full step",
+        "note": "no reference code exists (the paper ships none, BASELINE.json published = {}); the reference "
+                "arm is the CPU oracle timed on a bounded sample of the same workload",
     }
     print(json.dumps(line), flush=True)
 
