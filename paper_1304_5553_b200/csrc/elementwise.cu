@@ -6,10 +6,13 @@
 //   axpbyz: z[i] = a*x[i] + b*y[i]     12 B/elt fp32 (read x, y; write z)
 //   axpbz : z[i] = a*x[i] + b           8 B/elt fp32
 //
-// HBM-bound (0.25 flop/B).  B200 design: one CTA wave sized to full
-// residency (SMs x occupancy), 256-bit vector loads/stores (LDG/STG.256, one
-// 1 KiB contiguous request per warp instruction) with UNROLL independent
-// vectors per thread in flight, L1 bypassed (data is touched once).  A scalar
+// HBM-bound (0.25 flop/B).  B200 design: a one-shot grid (no grid-stride
+// wave) where CTA b owns the contiguous chunk of EW_BLOCK*UNROLL 32-byte
+// vectors starting at b*EW_BLOCK*UNROLL; 256-bit vector loads/stores
+// (LDG/STG.256, one 1 KiB contiguous request per warp instruction), all
+// UNROLL vectors of a thread loaded before any is used, L1 bypassed (data is
+// touched once).  tools/lab/ew_lab.cu measured this shape at 7.0 TB/s against
+// 6.3-6.5 TB/s for a persistent grid-stride wave (n = 2^28 fp32).  A scalar
 // head peels x/y/z to 32-byte alignment and a scalar tail finishes the
 // remainder; arrays whose addresses differ modulo 32 B take a scalar path.
 #include <cuda_runtime.h>
@@ -23,7 +26,7 @@
 namespace ga {
 namespace {
 
-constexpr int EW_BLOCK = 256;
+constexpr int EW_BLOCK = 512;
 
 template <typename T>
 struct EwArgs {
@@ -47,7 +50,6 @@ template <typename T, bool HAS_Y, int UNROLL, bool NC>
 __global__ void __launch_bounds__(EW_BLOCK) ew_vec_kernel(EwArgs<T> p) {
   constexpr int VEC = 32 / sizeof(T);
   const int64_t tid = (int64_t)blockIdx.x * EW_BLOCK + threadIdx.x;
-  const int64_t nthreads = (int64_t)gridDim.x * EW_BLOCK;
 
   // Scalar head (to 32 B alignment) and tail (remainder of the body).
   const int64_t tail0 = p.head + p.nvec * VEC;
@@ -65,13 +67,14 @@ __global__ void __launch_bounds__(EW_BLOCK) ew_vec_kernel(EwArgs<T> p) {
   const char *yb = HAS_Y ? reinterpret_cast<const char *>(p.y + p.head) : nullptr;
   char *zb = reinterpret_cast<char *>(p.z + p.head);
 
-  // Vector v of the body is handled by thread v mod nthreads; UNROLL vectors
-  // nthreads apart are loaded before any is used.
-  for (int64_t base = tid; base < p.nvec; base += nthreads * UNROLL) {
+  // CTA b owns vectors [b*CHUNK, (b+1)*CHUNK), CHUNK = EW_BLOCK*UNROLL; the
+  // loop only repeats if the grid was capped (n beyond 2^31 CTAs' worth).
+  constexpr int64_t CHUNK = (int64_t)EW_BLOCK * UNROLL;
+  for (int64_t base = (int64_t)blockIdx.x * CHUNK + threadIdx.x; base < p.nvec; base += (int64_t)gridDim.x * CHUNK) {
     V32 vx[UNROLL], vy[UNROLL];
 #pragma unroll
     for (int j = 0; j < UNROLL; ++j) {
-      int64_t v = base + j * nthreads;
+      int64_t v = base + j * EW_BLOCK;
       if (v < p.nvec) {
         vx[j] = ld_vec<NC>(xb + v * 32);
         if constexpr (HAS_Y) vy[j] = ld_vec<NC>(yb + v * 32);
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(EW_BLOCK) ew_vec_kernel(EwArgs<T> p) {
     }
 #pragma unroll
     for (int j = 0; j < UNROLL; ++j) {
-      int64_t v = base + j * nthreads;
+      int64_t v = base + j * EW_BLOCK;
       if (v < p.nvec) {
         V32 vz;
 #pragma unroll
@@ -119,6 +122,7 @@ ga_status_t launch_ew(int64_t n, const ga_scalar_t &a, const void *x, const ga_s
                       void *z, cudaStream_t s) {
   constexpr int VEC = 32 / sizeof(T);
   constexpr int UNROLL = HAS_Y ? 2 : 4;
+  constexpr int64_t CHUNK = (int64_t)EW_BLOCK * UNROLL;
   EwArgs<T> p;
   p.n = n;
   p.a = scalar_value<T>(a);
@@ -144,11 +148,7 @@ ga_status_t launch_ew(int64_t n, const ga_scalar_t &a, const void *x, const ga_s
   // In-place (z == x or z == y) must use coherent loads: the .nc path
   // requires the data to stay unwritten for the kernel's lifetime.
   const bool inplace = z == x || (HAS_Y && z == y);
-  const void *kern = inplace ? (const void *)ew_vec_kernel<T, HAS_Y, UNROLL, false>
-                             : (const void *)ew_vec_kernel<T, HAS_Y, UNROLL, true>;
-  const int max_grid = resident_grid(kern, EW_BLOCK);
-  int64_t want = std::max<int64_t>(cdiv(p.nvec, EW_BLOCK), 1);
-  int grid = (int)std::min<int64_t>(want, max_grid);
+  int grid = (int)std::min<int64_t>(std::max<int64_t>(cdiv(p.nvec, CHUNK), 1), 0x7fffffffLL);
   if (inplace) ew_vec_kernel<T, HAS_Y, UNROLL, false><<<grid, EW_BLOCK, 0, s>>>(p);
   else ew_vec_kernel<T, HAS_Y, UNROLL, true><<<grid, EW_BLOCK, 0, s>>>(p);
   count_launch();
