@@ -1049,6 +1049,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T> p) {
     if ((int64_t)t == p.num_tiles - 1) *p.ticket = (unsigned long long)((e + 1u) & EPOCH_MASK) << 32;
     s_tile = t;
     s_epoch = e;
+    if (p.trace) p.trace[(int64_t)t * 8 + 0] = globaltimer_ns();
   }
   __syncthreads();
   const int64_t tile = s_tile;
@@ -1107,6 +1108,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T> p) {
     }
     const T total = __shfl_sync(0xffffffffu, w, WARPS - 1);
     T prefix;
+    if (p.trace && lane == 0) p.trace[tile * 8 + 1] = globaltimer_ns();
     if (tile == 0) {
       prefix = T(0);
       if (lane == 0)
@@ -1118,6 +1120,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T> p) {
       prefix = look_back<T, DEPTH, 0>(p.status, tile, epoch);
       if (lane == 0) p.status.publish(tile, epoch, FLAG_INCLUSIVE, e_add(prefix, total));
     }
+    if (p.trace && lane == 0) p.trace[tile * 8 + 2] = globaltimer_ns();
     if (lane < WARPS) s_slice[lane] = e_add(prefix, e_sub(w, mine));  // exclusive prefix of slice `lane`
   }
   __syncthreads();
@@ -1159,6 +1162,209 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T> p) {
 #pragma unroll
         for (int k = 0; k < E; ++k)
           if (i + k < p.n) p.out[i + k] = o[k];
+      }
+    }
+  }
+  if (p.trace && threadIdx.x == 0) p.trace[tile * 8 + 3] = globaltimer_ns();
+}
+
+
+// ===========================================================================
+// Pipelined two-touch variant (persistent, warp-specialized, one CTA per SM).
+//   RW reader warps   : stream super-tile k+1 from HBM and sum its RW slices
+//                       (phase 1), claiming the next id one iteration ahead;
+//   1 look-back warp  : turns the slice sums of k+1 into the AGGREGATE,
+//                       publishes it, looks back, publishes INCLUSIVE and the
+//                       per-slice exclusive prefixes;
+//   RW writer warps   : re-read super-tile k from L2, scan it and store
+//                       (phase 3).
+// Phase 1 of one super-tile, the look-back of the next and phase 3 of the
+// previous overlap inside every SM, so HBM sees reads and writes all the
+// time and look-back latency hides behind the writers.  Hand-off through two
+// shared-memory buffers guarded by sequence flags.
+// ===========================================================================
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void st_volatile_shared(uint32_t *p, uint32_t v) {
+  asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(tma::smem_u32(p)), "r"(v) : "memory");
+}
+
+template <typename T, int RW, int ROWS, int RU, int WU, int DEPTH, bool NC, bool EXCLUSIVE>
+__global__ void __launch_bounds__((2 * RW + 1) * 32, 1) scan_pipe_kernel(ScanArgs<T> p) {
+  using namespace tma;
+  constexpr int E = Chunk<T>::E;
+  constexpr int ROW = 32 * E;  // elements per 512-byte row
+  constexpr int64_t SLICE = (int64_t)ROWS * ROW;
+  constexpr int64_t TILE = (int64_t)RW * SLICE;
+  static_assert(ROWS % RU == 0 && ROWS % WU == 0, "ROWS must be a multiple of the unrolls");
+  static_assert(RW <= 32, "slice sums are scanned by one warp");
+  __shared__ long long s_tile[2];
+  __shared__ T s_sums[2][RW];
+  __shared__ T s_off[2][RW];
+  __shared__ uint32_t sums_ready[2], prefix_ready[2], buf_free[2];
+  __shared__ uint32_t s_epoch;
+  __shared__ long long s_next;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t last_claim = p.num_tiles + (int64_t)gridDim.x - 1;
+
+  if (threadIdx.x == 0) {
+    sums_ready[0] = sums_ready[1] = prefix_ready[0] = prefix_ready[1] = buf_free[0] = buf_free[1] = 0u;
+  }
+  __syncthreads();
+
+  auto load_row = [&](long long tile, int slice, int r, uint64_t pol, bool full, T (&v)[E]) {
+    const int64_t i = (int64_t)tile * TILE + slice * SLICE + (int64_t)r * ROW + lane * E;
+    if (full) {
+      Chunk<T>::unpack(l2::ldg128_hint<NC>(p.in + i, pol), v);
+    } else {
+#pragma unroll
+      for (int k = 0; k < E; ++k) v[k] = i + k < p.n ? p.in[i + k] : T(0);
+    }
+  };
+  // one claim: returns the tile id or -1; resets the ticket on the globally last claim
+  auto claim = [&]() -> long long {
+    const unsigned long long old = atomicAdd(p.ticket, 1ull);
+    const int64_t t = (int64_t)(uint32_t)old;
+    const uint32_t e = (uint32_t)(old >> 32) & EPOCH_MASK;
+    s_epoch = e;
+    if (t == last_claim) *p.ticket = (unsigned long long)((e + 1u) & EPOCH_MASK) << 32;
+    return t < p.num_tiles ? (long long)t : -1ll;
+  };
+
+  if (warp < RW) {
+    // ------------------------------------------------ readers (phase 1)
+    const uint64_t keep = l2::policy_evict_last();
+    long long next = -1;
+    if (threadIdx.x == 0) next = claim();
+    for (uint32_t k = 0;; ++k) {
+      const int buf = k & 1;
+      if (k >= 2) wait_flag(&buf_free[buf], k - 1);
+      if (threadIdx.x == 0) {
+        s_tile[buf] = next;
+        // claim the following id now; its latency overlaps this phase
+        s_next = next >= 0 ? claim() : -1ll;
+      }
+      named_bar(1, RW * 32);
+      const long long t = s_tile[buf];
+      if (threadIdx.x == 0) next = s_next;
+      if (t < 0) {
+        if (threadIdx.x == 0) {
+          __threadfence_block();
+          st_volatile_shared(&sums_ready[buf], k + 1);
+        }
+        return;
+      }
+      const bool full = (int64_t)(t + 1) * TILE <= p.n;
+      T acc = T(0);
+#pragma unroll 1
+      for (int r0 = 0; r0 < ROWS; r0 += RU) {
+        T v[RU][E];
+#pragma unroll
+        for (int u = 0; u < RU; ++u) load_row(t, warp, r0 + u, keep, full, v[u]);
+#pragma unroll
+        for (int u = 0; u < RU; ++u)
+#pragma unroll
+          for (int q = 0; q < E; ++q) acc = e_add(acc, v[u][q]);
+      }
+      acc = warp_sum<T>(acc);
+      if (lane == 0) s_sums[buf][warp] = acc;
+      named_bar(1, RW * 32);
+      if (threadIdx.x == 0) {
+        __threadfence_block();
+        st_volatile_shared(&sums_ready[buf], k + 1);
+      }
+    }
+  } else if (warp == RW) {
+    // ------------------------------------------------ look-back warp
+    for (uint32_t k = 0;; ++k) {
+      const int buf = k & 1;
+      wait_flag(&sums_ready[buf], k + 1);
+      const long long t = s_tile[buf];
+      if (t < 0) {
+        if (lane == 0) {
+          __threadfence_block();
+          st_volatile_shared(&prefix_ready[buf], k + 1);
+        }
+        return;
+      }
+      const uint32_t epoch = s_epoch;
+      const T mine = lane < RW ? s_sums[buf][lane] : T(0);
+      T w = mine;
+#pragma unroll
+      for (int o = 1; o < RW; o <<= 1) {
+        const T u = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w = e_add(w, u);
+      }
+      const T total = __shfl_sync(0xffffffffu, w, RW - 1);
+      T prefix;
+      if (t == 0) {
+        prefix = T(0);
+        if (lane == 0)
+          for (int64_t c = 0; c < p.carry_count; ++c) prefix = e_add(prefix, p.carry[c]);
+        prefix = __shfl_sync(0xffffffffu, prefix, 0);
+        if (lane == 0) p.status.publish(0, epoch, FLAG_INCLUSIVE, e_add(prefix, total));
+      } else {
+        if (lane == 0) p.status.publish(t, epoch, FLAG_AGGREGATE, total);
+        prefix = look_back<T, DEPTH, 0>(p.status, t, epoch);
+        if (lane == 0) p.status.publish(t, epoch, FLAG_INCLUSIVE, e_add(prefix, total));
+      }
+      if (lane < RW) s_off[buf][lane] = e_add(prefix, e_sub(w, mine));
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        st_volatile_shared(&prefix_ready[buf], k + 1);
+      }
+    }
+  } else {
+    // ------------------------------------------------ writers (phase 3)
+    const int slice = warp - RW - 1;
+    const uint64_t drop = l2::policy_evict_first();
+    for (uint32_t k = 0;; ++k) {
+      const int buf = k & 1;
+      wait_flag(&prefix_ready[buf], k + 1);
+      const long long t = s_tile[buf];
+      if (t < 0) return;
+      const bool full = (int64_t)(t + 1) * TILE <= p.n;
+      T base = s_off[buf][slice];
+#pragma unroll 1
+      for (int r0 = 0; r0 < ROWS; r0 += WU) {
+        T v[WU][E];
+#pragma unroll
+        for (int u = 0; u < WU; ++u) load_row(t, slice, r0 + u, drop, full, v[u]);
+#pragma unroll
+        for (int u = 0; u < WU; ++u) {
+#pragma unroll
+          for (int q = 1; q < E; ++q) v[u][q] = e_add(v[u][q], v[u][q - 1]);
+          const T tot = v[u][E - 1];
+          T x = tot;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const T y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x = e_add(x, y);
+          }
+          const T cb = e_add(base, e_sub(x, tot));
+          base = e_add(base, __shfl_sync(0xffffffffu, x, 31));
+          T o[E];
+#pragma unroll
+          for (int q = 0; q < E; ++q) {
+            if constexpr (EXCLUSIVE) o[q] = q == 0 ? cb : e_add(cb, v[u][q - 1]);
+            else o[q] = e_add(cb, v[u][q]);
+          }
+          const int64_t i = (int64_t)t * TILE + slice * SLICE + (int64_t)(r0 + u) * ROW + lane * E;
+          if (full) {
+            l2::stg128_hint(p.out + i, Chunk<T>::pack(o), drop);
+          } else {
+#pragma unroll
+            for (int q = 0; q < E; ++q)
+              if (i + q < p.n) p.out[i + q] = o[q];
+          }
+        }
+      }
+      named_bar(2, RW * 32);
+      if (slice == 0 && lane == 0) {
+        __threadfence_block();
+        st_volatile_shared(&buf_free[buf], k + 1);
       }
     }
   }

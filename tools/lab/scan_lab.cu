@@ -8,6 +8,9 @@
 
 using namespace ga::scan_detail;
 
+static unsigned long long *g_trace = nullptr;
+extern "C" void lab_set_trace(void *p) { g_trace = (unsigned long long *)p; }
+
 template <typename T, int BLOCK, int ITEMS, int DEPTH, int BO>
 static int run(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   ScanArgs<T> p = make_args<T>(n, (int64_t)BLOCK * ITEMS, in, out, nullptr, 0, ws);
@@ -41,8 +44,6 @@ static int run_smem(int64_t n, const void *in, void *out, void *ws, cudaStream_t
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
-static unsigned long long *g_trace = nullptr;
-extern "C" void lab_set_trace(void *p) { g_trace = (unsigned long long *)p; }
 
 template <typename T, int C, int CH, int STAGES, int DEPTH, int NL, int CPS>
 static int run_ws(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
@@ -66,6 +67,7 @@ template <typename T, int WARPS, int ROWS, int UNROLL, int DEPTH, int HINTS>
 static int run_l2(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   constexpr int64_t TILE = (int64_t)WARPS * ROWS * 512 / sizeof(T);
   ScanArgs<T> p = make_args<T>(n, TILE, in, out, nullptr, 0, ws);
+  p.trace = g_trace;
   if (HINTS == 2) {  // parked in shared memory
     auto k = scan_l2_kernel<T, WARPS, ROWS, UNROLL, DEPTH, false, true, true, true>;
     const int smem = WARPS * ROWS * 512;
@@ -82,6 +84,31 @@ static int run_l2(int64_t n, const void *in, void *out, void *ws, cudaStream_t s
   return e == cudaSuccess ? 0 : 100 + (int)e;
 }
 
+template <typename T, int RW, int ROWS, int RU, int WU, int DEPTH>
+static int run_pipe(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
+  constexpr int64_t TILE = (int64_t)RW * ROWS * 512 / sizeof(T);
+  ScanArgs<T> p = make_args<T>(n, TILE, in, out, nullptr, 0, ws);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = sms;
+  if (grid > p.num_tiles) grid = p.num_tiles;
+  scan_pipe_kernel<T, RW, ROWS, RU, WU, DEPTH, true, true><<<(int)grid, (2 * RW + 1) * 32, 0, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : 100 + (int)e;
+}
+
+#define PIPE_VARIANTS(X)                       \
+  X(200, int32_t, 8, 64, 16, 8, 4)             \
+  X(201, int32_t, 8, 32, 16, 8, 4)             \
+  X(202, int32_t, 8, 64, 8, 8, 4)              \
+  X(203, int32_t, 12, 32, 16, 8, 4)            \
+  X(204, int32_t, 16, 32, 8, 8, 4)             \
+  X(205, int32_t, 8, 128, 16, 8, 4)            \
+  X(206, int32_t, 16, 16, 16, 8, 4)            \
+  X(220, int64_t, 8, 64, 16, 8, 4)             \
+  X(221, int64_t, 16, 32, 8, 8, 4)
+
 #define L2_VARIANTS(X)                       \
   X(140, int32_t, 16, 16, 8, 4, 1)           \
   X(141, int32_t, 16, 16, 8, 4, 0)           \
@@ -92,6 +119,17 @@ static int run_l2(int64_t n, const void *in, void *out, void *ws, cudaStream_t s
   X(146, int32_t, 16, 16, 4, 4, 1)           \
   X(147, int32_t, 16, 64, 8, 4, 1)           \
   X(148, int32_t, 16, 32, 8, 4, 0)           \
+  X(180, int32_t, 16, 32, 8, 8, 1)           \
+  X(181, int32_t, 16, 32, 8, 2, 1)           \
+  X(182, int32_t, 16, 24, 8, 4, 1)           \
+  X(183, int32_t, 16, 40, 8, 4, 1)           \
+  X(184, int32_t, 16, 48, 8, 4, 1)           \
+  X(185, int32_t, 12, 32, 8, 4, 1)           \
+  X(186, int32_t, 20, 32, 8, 4, 1)           \
+  X(187, int32_t, 24, 32, 8, 4, 1)           \
+  X(188, int32_t, 16, 36, 6, 4, 1)           \
+  X(189, int32_t, 16, 30, 10, 4, 1)          \
+  X(190, int32_t, 16, 32, 4, 4, 1)           \
   X(149, int32_t, 16, 32, 4, 4, 1)           \
   X(150, int32_t, 16, 64, 4, 4, 1)           \
   X(151, int32_t, 32, 32, 4, 4, 1)           \
@@ -184,6 +222,10 @@ extern "C" int lab_scan(int v, int64_t n, const void *in, void *out, void *ws, v
   case id: return run<T, B, I, D, BO>(n, in, out, ws, s);
     VARIANTS(CASE)
 #undef CASE
+#define PCASE(id, T, RW, R, RU, WU, D) \
+  case id: return run_pipe<T, RW, R, RU, WU, D>(n, in, out, ws, s);
+    PIPE_VARIANTS(PCASE)
+#undef PCASE
 #define LCASE(id, T, W, R, U, D, H) \
   case id: return run_l2<T, W, R, U, D, H>(n, in, out, ws, s);
     L2_VARIANTS(LCASE)
@@ -210,6 +252,10 @@ extern "C" int64_t lab_scan_tile(int v) {
   case id: return (int64_t)B * I;
     VARIANTS(TILE)
 #undef TILE
+#define PTILE(id, T, RW, R, RU, WU, D) \
+  case id: return (int64_t)RW * R * 512 / sizeof(T);
+    PIPE_VARIANTS(PTILE)
+#undef PTILE
 #define LTILE(id, T, W, R, U, D, H) \
   case id: return (int64_t)W * R * 512 / sizeof(T);
     L2_VARIANTS(LTILE)
@@ -230,4 +276,4 @@ extern "C" int64_t lab_scan_tile(int v) {
   return 0;
 }
 
-extern "C" int lab_scan_elem_bytes(int v) { return (v >= 20 && v < 40) || (v >= 60 && v < 78) || (v >= 90 && v < 100) || (v >= 120 && v < 140) || (v >= 160 && v < 170) || v >= 178 ? 8 : 4; }
+extern "C" int lab_scan_elem_bytes(int v) { return (v >= 20 && v < 40) || (v >= 60 && v < 78) || (v >= 90 && v < 100) || (v >= 120 && v < 140) || (v >= 160 && v < 170) || (v >= 178 && v < 180) || (v >= 191 && v < 200) || v >= 220 ? 8 : 4; }
