@@ -7,11 +7,12 @@
 // in flight stay L2-resident (scan_l2_kernel in scan_kernel.cuh):
 //   - CTA draws {epoch, super-tile id} with one 64-bit atomic (ids in CTA
 //     start order, so every predecessor is already running);
-//   - phase 1 streams its 256 KiB super-tile from HBM (each warp its own
-//     16 KiB slice, 8 x 512-byte rows in flight, L2 evict_last) and sums it;
-//     the AGGREGATE is published as soon as the sum is known;
-//   - phase 2: warp 0 looks back over 128 predecessors per round trip,
-//     stopping at the nearest INCLUSIVE, and publishes INCLUSIVE;
+//   - phase 1 streams its 384 KiB super-tile from HBM (each of 24 warps its
+//     own 16 KiB slice, 8 x 512-byte rows in flight, L2 evict_last) and sums
+//     it; the AGGREGATE is published as soon as the sum is known;
+//   - phase 2: warp 0 looks back over 256 predecessors per round trip,
+//     stopping at the nearest INCLUSIVE, and publishes INCLUSIVE; meanwhile
+//     the other warps already load and locally scan their first 8 rows;
 //   - phase 3 re-reads the slice (L2 hit, evict_first), scans it row by row
 //     (in-chunk serial scan + warp shuffle scan) and stores 512 B per warp
 //     instruction.
@@ -34,9 +35,11 @@ namespace {
 
 using namespace scan_detail;
 
-// Tuned super-tile shape (tools/lab/run_scan_lab.py): 16 warps x 32 rows of
-// 512 bytes = 256 KiB per CTA, 8 rows in flight per warp, 4-deep look-back.
-constexpr int L2_WARPS = 16, L2_ROWS = 32, L2_UNROLL = 8, L2_DEPTH = 4;
+// Tuned super-tile shape (tools/lab/run_scan_lab.py): 24 warps x 32 rows of
+// 512 bytes = 384 KiB per CTA (one CTA per SM), 8 rows in flight per warp,
+// 8-deep look-back (256 predecessors per round trip), and warps 1..23 load
+// and locally scan their first phase-3 rows while warp 0 looks back.
+constexpr int L2_WARPS = 24, L2_ROWS = 32, L2_UNROLL = 8, L2_DEPTH = 8;
 // Fallback for arrays that are not 16-byte aligned: register tile of
 // 256 threads x 16 scalar-loaded items.
 constexpr int RG_BLOCK = 256, RG_ITEMS = 16;
@@ -62,10 +65,10 @@ ga_status_t run(int64_t n, const void *in, void *out, const void *carry, int64_t
     ScanArgs<T> p = make_args<T>(n, l2_tile<T>(), in, out, carry, carry_count, ws);
     const int grid = (int)p.num_tiles;
     if (inplace)
-      scan_l2_kernel<T, L2_WARPS, L2_ROWS, L2_UNROLL, L2_DEPTH, true, false, EXCLUSIVE>
+      scan_l2_kernel<T, L2_WARPS, L2_ROWS, L2_UNROLL, L2_DEPTH, true, false, EXCLUSIVE, false, true>
           <<<grid, L2_WARPS * 32, 0, s>>>(p);
     else
-      scan_l2_kernel<T, L2_WARPS, L2_ROWS, L2_UNROLL, L2_DEPTH, true, true, EXCLUSIVE>
+      scan_l2_kernel<T, L2_WARPS, L2_ROWS, L2_UNROLL, L2_DEPTH, true, true, EXCLUSIVE, false, true>
           <<<grid, L2_WARPS * 32, 0, s>>>(p);
   } else {
     ScanArgs<T> p = make_args<T>(n, (int64_t)RG_BLOCK * RG_ITEMS, in, out, carry, carry_count, ws);

@@ -1029,9 +1029,11 @@ __device__ __forceinline__ void stg128_hint(void *p, const uint4 &v, uint64_t po
 
 // STAGE_SMEM: phase 1 also parks every row in shared memory (dynamic smem of
 // WARPS*ROWS*512 bytes) and phase 3 reads it from there instead of L2.
+// EARLY: warps 1..WARPS-1 load and locally scan their first UNROLL rows of
+// phase 3 while warp 0 is still in the look-back.
 template <typename T, int WARPS, int ROWS, int UNROLL, int DEPTH, bool HINTS, bool NC, bool EXCLUSIVE,
-          bool STAGE_SMEM = false>
-__global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T> p) {
+          bool STAGE_SMEM = false, bool EARLY = false, int MINB = 1>
+__global__ void __launch_bounds__(WARPS * 32, MINB) scan_l2_kernel(ScanArgs<T> p) {
   extern __shared__ __align__(128) uint8_t park[];
   using namespace tma;
   constexpr int E = Chunk<T>::E;
@@ -1123,18 +1125,16 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T> p) {
     if (p.trace && lane == 0) p.trace[tile * 8 + 2] = globaltimer_ns();
     if (lane < WARPS) s_slice[lane] = e_add(prefix, e_sub(w, mine));  // exclusive prefix of slice `lane`
   }
-  __syncthreads();
-  T base = s_slice[warp];
-
-  // phase 3: re-read (L2 or the parked copy), scan row by row, store
-#pragma unroll 1
-  for (int r0 = 0; r0 < ROWS; r0 += UNROLL) {
-    T v[UNROLL][E];
+  // phase 3: re-read (L2 or the parked copy), scan row by row, store.
+  // load_local: rows [r0, r0+UNROLL) into registers, in-row scans, and each
+  // row's exclusive offset relative to the chunk start (off) + chunk total.
+  auto load_local = [&](int r0, T (&v)[UNROLL][E], T (&off)[UNROLL], T &ctot) {
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
       if constexpr (STAGE_SMEM) Chunk<T>::unpack(lds128(my_park + (r0 + u) * 512), v[u]);
       else load_row(r0 + u, drop, v[u]);
     }
+    ctot = T(0);
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
 #pragma unroll
@@ -1146,8 +1146,14 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T> p) {
         const T y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x = e_add(x, y);
       }
-      const T cb = e_add(base, e_sub(x, tot));
-      base = e_add(base, __shfl_sync(0xffffffffu, x, 31));
+      off[u] = e_add(ctot, e_sub(x, tot));
+      ctot = e_add(ctot, __shfl_sync(0xffffffffu, x, 31));
+    }
+  };
+  auto store_chunk = [&](int r0, const T (&v)[UNROLL][E], const T (&off)[UNROLL], T base) {
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const T cb = e_add(base, off[u]);
       T o[E];
 #pragma unroll
       for (int k = 0; k < E; ++k) {
@@ -1164,10 +1170,24 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T> p) {
           if (i + k < p.n) p.out[i + k] = o[k];
       }
     }
+  };
+  T v0[UNROLL][E], off0[UNROLL], ctot0;
+  const bool early = EARLY && warp != 0;
+  if (early) load_local(0, v0, off0, ctot0);
+  __syncthreads();
+  T base = s_slice[warp];
+  if (!early) load_local(0, v0, off0, ctot0);
+  store_chunk(0, v0, off0, base);
+  base = e_add(base, ctot0);
+#pragma unroll 1
+  for (int r0 = UNROLL; r0 < ROWS; r0 += UNROLL) {
+    T v[UNROLL][E], off[UNROLL], ctot;
+    load_local(r0, v, off, ctot);
+    store_chunk(r0, v, off, base);
+    base = e_add(base, ctot);
   }
   if (p.trace && threadIdx.x == 0) p.trace[tile * 8 + 3] = globaltimer_ns();
 }
-
 
 // ===========================================================================
 // Pipelined two-touch variant (persistent, warp-specialized, one CTA per SM).

@@ -41,7 +41,7 @@ def main():
     ws = torch.zeros(256 + 32 * n // 64 + (1 << 20), dtype=torch.uint8, device=dev)
     s = torch.cuda.current_stream().cuda_stream
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for v in [142] + list(range(180, 191)):
+    for v in [142, 232, 161] + list(range(240, 250)):
         if only and v not in only:
             continue
         is64 = L.lab_scan_elem_bytes(v) == 8

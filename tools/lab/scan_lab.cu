@@ -78,6 +78,10 @@ static int run_l2(int64_t n, const void *in, void *out, void *ws, cudaStream_t s
     const int smem = WARPS * ROWS * 512;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k<<<(int)p.num_tiles, WARPS * 32, smem, s>>>(p);
+  } else if (HINTS == 5) {  // early + 2 CTAs/SM forced
+    scan_l2_kernel<T, WARPS, ROWS, UNROLL, DEPTH, true, true, true, false, true, 2><<<(int)p.num_tiles, WARPS * 32, 0, s>>>(p);
+  } else if (HINTS == 4) {  // early phase-3 loads during the look-back
+    scan_l2_kernel<T, WARPS, ROWS, UNROLL, DEPTH, true, true, true, false, true><<<(int)p.num_tiles, WARPS * 32, 0, s>>>(p);
   } else
   scan_l2_kernel<T, WARPS, ROWS, UNROLL, DEPTH, HINTS != 0, true, true><<<(int)p.num_tiles, WARPS * 32, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();
@@ -119,6 +123,23 @@ static int run_pipe(int64_t n, const void *in, void *out, void *ws, cudaStream_t
   X(146, int32_t, 16, 16, 4, 4, 1)           \
   X(147, int32_t, 16, 64, 8, 4, 1)           \
   X(148, int32_t, 16, 32, 8, 4, 0)           \
+  X(240, int32_t, 16, 32, 8, 4, 5)           \
+  X(241, int32_t, 16, 32, 4, 4, 5)           \
+  X(242, int32_t, 32, 16, 4, 4, 4)           \
+  X(243, int32_t, 24, 40, 8, 4, 4)           \
+  X(244, int32_t, 24, 24, 8, 4, 4)           \
+  X(245, int32_t, 32, 16, 8, 4, 4)           \
+  X(246, int32_t, 16, 48, 8, 4, 5)           \
+  X(247, int32_t, 24, 32, 8, 8, 4)           \
+  X(248, int64_t, 24, 32, 8, 4, 4)           \
+  X(249, int64_t, 16, 32, 8, 4, 5)           \
+  X(230, int32_t, 16, 32, 8, 4, 4)           \
+  X(231, int32_t, 16, 24, 8, 4, 4)           \
+  X(232, int32_t, 24, 32, 8, 4, 4)           \
+  X(233, int32_t, 16, 32, 8, 2, 4)           \
+  X(234, int32_t, 16, 16, 8, 4, 4)           \
+  X(235, int64_t, 16, 32, 8, 4, 4)           \
+  X(236, int64_t, 16, 16, 8, 4, 4)           \
   X(180, int32_t, 16, 32, 8, 8, 1)           \
   X(181, int32_t, 16, 32, 8, 2, 1)           \
   X(182, int32_t, 16, 24, 8, 4, 1)           \
@@ -276,4 +297,4 @@ extern "C" int64_t lab_scan_tile(int v) {
   return 0;
 }
 
-extern "C" int lab_scan_elem_bytes(int v) { return (v >= 20 && v < 40) || (v >= 60 && v < 78) || (v >= 90 && v < 100) || (v >= 120 && v < 140) || (v >= 160 && v < 170) || (v >= 178 && v < 180) || (v >= 191 && v < 200) || v >= 220 ? 8 : 4; }
+extern "C" int lab_scan_elem_bytes(int v) { return (v >= 20 && v < 40) || (v >= 60 && v < 78) || (v >= 90 && v < 100) || (v >= 120 && v < 140) || (v >= 160 && v < 170) || (v >= 178 && v < 180) || (v >= 191 && v < 200) || (v >= 220 && v < 230) || v == 235 || v == 236 || v == 248 || v == 249 ? 8 : 4; }
