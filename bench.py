@@ -208,10 +208,18 @@ def main():
     from paper_1304_5553_b200 import dist as gdist
     from paper_1304_5553_b200 import gpuarray as G
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # BENCH_SHARE_GPU=1 (testing only): every rank uses cuda:0 and gloo, so the
+    # N > 1 choreography can be exercised on a one-GPU box; numbers from such a
+    # run are not bench values.
+    share = os.environ.get("BENCH_SHARE_GPU") == "1"
+    dev_index = 0 if share else local_rank
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     n = 1 << args.log2n
     start = rank * n  # weak scaling: shard g = global [g*n, (g+1)*n)
     x = synth.device_fill(synth.F32_U01, synth.SEED_X, n, start=start, device=dev)
@@ -255,7 +263,7 @@ def main():
         step(False)
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(dev_index)
     clocks.start()
     time.sleep(0.3)  # let the sampler start
     if world > 1:

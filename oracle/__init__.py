@@ -69,6 +69,14 @@ def lib():
         L.oracle_scan_i32.argtypes = [ctypes.c_int, i64, vp, vp, i32]
         L.oracle_scan_i64.restype = None
         L.oracle_scan_i64.argtypes = [ctypes.c_int, i64, vp, vp, i64]
+        L.oracle_scan_maxmin_f32.restype = None
+        L.oracle_scan_maxmin_f32.argtypes = [ctypes.c_int, ctypes.c_int, i64, vp, vp, f32]
+        L.oracle_scan_maxmin_f64.restype = None
+        L.oracle_scan_maxmin_f64.argtypes = [ctypes.c_int, ctypes.c_int, i64, vp, vp, d]
+        L.oracle_scan_maxmin_int.restype = None
+        L.oracle_scan_maxmin_int.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, i64, vp, vp, i64]
+        L.oracle_scan_sum_float.restype = None
+        L.oracle_scan_sum_float.argtypes = [ctypes.c_int, ctypes.c_int, i64, vp, vp, d, vp]
         _lib = L
     return _lib
 
@@ -137,11 +145,38 @@ def reduce(op, map_, x, y=None, out_dtype=None, return_sumabs=False):
     return (r, None) if return_sumabs else r
 
 
-def scan(kind, x, carry=0, out=None):
-    """Prefix sum; exclusive head = carry (neutral 0 by default)."""
+NEUTRAL = {
+    (MAX, np.dtype(np.float32)): -np.inf, (MIN, np.dtype(np.float32)): np.inf,
+    (MAX, np.dtype(np.float64)): -np.inf, (MIN, np.dtype(np.float64)): np.inf,
+    (MAX, np.dtype(np.int32)): np.iinfo(np.int32).min, (MIN, np.dtype(np.int32)): np.iinfo(np.int32).max,
+    (MAX, np.dtype(np.int64)): np.iinfo(np.int64).min, (MIN, np.dtype(np.int64)): np.iinfo(np.int64).max,
+}
+
+
+def scan(kind, x, carry=None, out=None, op=SUM, return_sumabs=False):
+    """Scan with reduction expression `op`; the exclusive
+    head / inclusive start is `carry` (default: the neutral element, R13).
+    Integer SUM wraps in the element type; float SUM returns the exact prefix
+    sums as float64 (and, with return_sumabs, |c| + sum |x_j| per position);
+    MAX / MIN fold with maxNum/minNum and return the element type."""
     x = _c(x)
+    L = lib()
+    if op == SUM and x.dtype.kind == "f":
+        res = np.empty(x.size, np.float64)
+        sa = np.empty(x.size, np.float64) if return_sumabs else None
+        L.oracle_scan_sum_float(kind, _DT[x.dtype], x.size, _ptr(x), _ptr(res), float(carry or 0.0), _ptr(sa))
+        return (res, sa) if return_sumabs else res
     if out is None:
         out = np.empty_like(x)
-    fn = {np.dtype(np.int32): lib().oracle_scan_i32, np.dtype(np.int64): lib().oracle_scan_i64}[x.dtype]
-    fn(kind, x.size, _ptr(x), _ptr(out), int(np.array(carry).astype(x.dtype)))
+    if op == SUM:
+        fn = {np.dtype(np.int32): L.oracle_scan_i32, np.dtype(np.int64): L.oracle_scan_i64}[x.dtype]
+        fn(kind, x.size, _ptr(x), _ptr(out), int(np.array(carry or 0).astype(x.dtype)))
+        return out
+    c = NEUTRAL[(op, x.dtype)] if carry is None else carry
+    if x.dtype == np.float32:
+        L.oracle_scan_maxmin_f32(op, kind, x.size, _ptr(x), _ptr(out), float(c))
+    elif x.dtype == np.float64:
+        L.oracle_scan_maxmin_f64(op, kind, x.size, _ptr(x), _ptr(out), float(c))
+    else:
+        L.oracle_scan_maxmin_int(op, kind, _DT[x.dtype], x.size, _ptr(x), _ptr(out), int(c))
     return out

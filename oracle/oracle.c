@@ -266,3 +266,78 @@ void oracle_scan_i64(int kind, int64_t n, const int64_t *in, int64_t *out, int64
     }
   }
 }
+
+/* ------------------------------------------------------------------------ */
+/* Scan with the other reduction expressions and element types (§8(f)        */
+/* NEXT-2; the paper's scan facility takes a "scan expression" like the      */
+/* reduction's, P:496-499 with P:479-485).                                    */
+/*   MAX / MIN, any dtype: running fold from the neutral element (or the     */
+/*     carry-in), maxNum/minNum for floats (R6) — exact.                      */
+/*   SUM over floats: the exact prefix sums S_i = c + x_0 + ... + x_i,        */
+/*     accumulated with Neumaier compensation in float64 and returned as      */
+/*     float64 (the GPU's tree/look-back order is an approximation of them;   */
+/*     DESIGN.md R22 gives the tolerance).  sumabs_out[i] = |c| + sum|x_j|.   */
+/* ------------------------------------------------------------------------ */
+void oracle_scan_maxmin_f32(int op, int kind, int64_t n, const float *in, float *out, float carry) {
+  float acc = carry;
+  for (int64_t i = 0; i < n; ++i) {
+    float v = in[i];
+    if (kind == O_INCLUSIVE) {
+      acc = (op == O_MAX) ? fmaxf(acc, v) : fminf(acc, v);
+      out[i] = acc;
+    } else {
+      out[i] = acc;
+      acc = (op == O_MAX) ? fmaxf(acc, v) : fminf(acc, v);
+    }
+  }
+}
+
+void oracle_scan_maxmin_f64(int op, int kind, int64_t n, const double *in, double *out, double carry) {
+  double acc = carry;
+  for (int64_t i = 0; i < n; ++i) {
+    double v = in[i];
+    if (kind == O_INCLUSIVE) {
+      acc = (op == O_MAX) ? fmax(acc, v) : fmin(acc, v);
+      out[i] = acc;
+    } else {
+      out[i] = acc;
+      acc = (op == O_MAX) ? fmax(acc, v) : fmin(acc, v);
+    }
+  }
+}
+
+void oracle_scan_maxmin_int(int op, int kind, int dt, int64_t n, const void *in, void *out, int64_t carry) {
+  int64_t acc = carry;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t v = (dt == O_I32) ? (int64_t)((const int32_t *)in)[i] : ((const int64_t *)in)[i];
+    if (kind == O_INCLUSIVE) {
+      if (op == O_MAX) { if (v > acc) acc = v; }
+      else { if (v < acc) acc = v; }
+    }
+    if (dt == O_I32) ((int32_t *)out)[i] = (int32_t)acc;
+    else ((int64_t *)out)[i] = acc;
+    if (kind == O_EXCLUSIVE) {
+      if (op == O_MAX) { if (v > acc) acc = v; }
+      else { if (v < acc) acc = v; }
+    }
+  }
+}
+
+void oracle_scan_sum_float(int kind, int dt, int64_t n, const void *in, double *out, double carry,
+                           double *sumabs_out) {
+  neumaier_t acc = {carry, 0.0};
+  neumaier_t abs_acc = {fabs(carry), 0.0};
+  for (int64_t i = 0; i < n; ++i) {
+    double v = (dt == O_F32) ? (double)((const float *)in)[i] : ((const double *)in)[i];
+    if (kind == O_INCLUSIVE) {
+      neumaier_add(&acc, v);
+      neumaier_add(&abs_acc, fabs(v));
+    }
+    out[i] = acc.s + acc.c;
+    if (sumabs_out) sumabs_out[i] = abs_acc.s + abs_acc.c;
+    if (kind == O_EXCLUSIVE) {
+      neumaier_add(&acc, v);
+      neumaier_add(&abs_acc, fabs(v));
+    }
+  }
+}

@@ -353,3 +353,66 @@ def test_scan_reduce_consistency_and_inplace():
 
 def test_scan_empty():
     assert oracle.scan(oracle.INCLUSIVE, np.zeros(0, np.int32)).size == 0
+
+
+# ------------------------------------------------------------ scans with MAX/MIN and float SUM (NEXT-2)
+@pytest.mark.parametrize("dt", [np.int32, np.int64, np.float32, np.float64])
+@pytest.mark.parametrize("op", [oracle.MAX, oracle.MIN])
+def test_scan_maxmin_match_numpy_accumulate(dt, op):
+    """Running max/min = numpy.fmax/fmin.accumulate (NaN-ignoring, R6);
+    exclusive = the same shifted right with the neutral element at the head."""
+    if np.dtype(dt).kind == "f":
+        x = RNG.standard_normal(10007).astype(dt)
+        x[[5, 77, 4000]] = np.nan
+        acc = np.fmax.accumulate if op == oracle.MAX else np.fmin.accumulate
+        neutral = -np.inf if op == oracle.MAX else np.inf
+    else:
+        info = np.iinfo(dt)
+        x = RNG.integers(info.min, info.max, size=10007, dtype=dt, endpoint=True)
+        acc = np.maximum.accumulate if op == oracle.MAX else np.minimum.accumulate
+        neutral = info.min if op == oracle.MAX else info.max
+    inc = acc(np.concatenate([np.array([neutral], dt), x]))[1:].astype(dt)  # fold from the neutral
+    assert bits_equal(oracle.scan(oracle.INCLUSIVE, x, op=op), inc)
+    exc = np.concatenate([np.array([neutral], dt), inc[:-1]])
+    assert bits_equal(oracle.scan(oracle.EXCLUSIVE, x, op=op), exc)
+
+
+def test_scan_max_spec_like_example():
+    x = np.array([3, 1, 4, 1, 5, 9, 2, 6], np.int32)
+    assert oracle.scan(oracle.INCLUSIVE, x, op=oracle.MAX).tolist() == [3, 3, 4, 4, 5, 9, 9, 9]
+    assert oracle.scan(oracle.EXCLUSIVE, x, op=oracle.MIN).tolist() == [2147483647, 3, 1, 1, 1, 1, 1, 1]
+    assert oracle.scan(oracle.INCLUSIVE, x, op=oracle.MAX, carry=7).tolist() == [7, 7, 7, 7, 7, 9, 9, 9]
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_scan_float_sum_exact_prefixes(dt):
+    """Float SUM scan returns the exact prefix sums (as float64): equal to
+    math.fsum of every prefix at sampled points (catches an uncompensated
+    running sum, an off-by-one head, a dropped carry)."""
+    x = synth.host_fill(synth.F32_S11 if dt == np.float32 else synth.F64_S11, 9, 50_001)
+    x[100] = 1e20
+    x[101] = -1e20  # cancellation a plain running double sum would get wrong
+    inc, sa = oracle.scan(oracle.INCLUSIVE, x, return_sumabs=True)
+    exc = oracle.scan(oracle.EXCLUSIVE, x, carry=0.25)
+    u = 2.0 ** -53
+    for i in (0, 1, 99, 100, 101, 102, 4095, 50_000):
+        pref = math.fsum(float(v) for v in x[:i + 1])
+        sabs = math.fsum(abs(float(v)) for v in x[:i + 1])
+        # Neumaier's bound: 2u|S| + 2 i u^2 sum|x| (the 1e20 terms make the second visible)
+        assert abs(inc[i] - pref) <= 2 * u * abs(pref) + 2 * (i + 1) * u * u * sabs + 1e-300
+        assert sa[i] == pytest.approx(sabs, rel=1e-15)
+        pe = math.fsum([0.25] + [float(v) for v in x[:i]])
+        assert abs(exc[i] - pe) <= 2 * u * abs(pe) + 2 * (i + 1) * u * u * (sabs + 0.25) + 1e-300
+    # a plain running float64 sum is visibly worse right after the cancellation
+    plain = np.cumsum(x.astype(np.float64))
+    exact = math.fsum(float(v) for v in x[:102])
+    assert abs(plain[101] - exact) > abs(inc[101] - exact)
+
+
+def test_scan_float_sum_closed_forms():
+    n = 1 << 20
+    ones = np.ones(n, np.float32)
+    assert np.array_equal(oracle.scan(oracle.INCLUSIVE, ones), np.arange(1, n + 1, dtype=np.float64))
+    r = synth.host_fill(synth.F64_RAMP, 0, n)
+    i = np.arange(n, dtype=np.float64)
+    assert np.array_equal(oracle.scan(oracle.EXCLUSIVE, r), i * (i - 1) / 2)
