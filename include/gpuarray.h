@@ -123,14 +123,17 @@ ga_status_t gpuarray_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype
  * error at the next synchronisation) after 10 s instead of hanging. */
 size_t gpuarray_scan_workspace_bytes(ga_dtype_t dt, int64_t n);
 
-/* Prefix sum with "+" (op must be GA_OP_SUM), dt in {I32, I64}:
- *   inclusive: out[i] = c + in[0] + ... + in[i]
- *   exclusive: out[0] = c, out[i] = c + in[0] + ... + in[i-1]   (R13)
- * where c = carry[0] + ... + carry[carry_count-1] (a device array of dt; c = 0,
- * the neutral element, when carry_count == 0).  The carry is how a sharded
+/* Scan with the reduction expression op ∈ {SUM, MAX, MIN} (written ⊕ below),
+ * dt in {F32, F64, I32, I64}:
+ *   inclusive: out[i] = c ⊕ in[0] ⊕ ... ⊕ in[i]
+ *   exclusive: out[0] = c, out[i] = c ⊕ in[0] ⊕ ... ⊕ in[i-1]   (R13)
+ * where c = carry[0] ⊕ ... ⊕ carry[carry_count-1] (a device array of dt; c is
+ * the neutral element when carry_count == 0).  The carry is how a sharded
  * scan passes the totals of earlier shards.  Integers
- * wrap (R4, R14).  out may equal in (in-place); other overlap is invalid.
- * n == 0: no-op. */
+ * wrap (R4, R14); MAX/MIN are exact (maxNum/minNum for floats, R6); float
+ * SUM is a tree/look-back-ordered approximation of the exact prefix sums
+ * (R22), not bit-reproducible run to run.  out may equal in
+ * (in-place); other overlap is invalid.  n == 0: no-op. */
 ga_status_t gpuarray_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_t n, const void *in,
                           void *out, const void *carry, int64_t carry_count, void *workspace,
                           size_t workspace_bytes, void *stream);

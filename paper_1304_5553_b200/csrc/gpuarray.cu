@@ -123,11 +123,10 @@ size_t gpuarray_scan_workspace_bytes(ga_dtype_t dt, int64_t n) { return n < 0 ? 
 ga_status_t gpuarray_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_t n, const void *in, void *out,
                           const void *carry, int64_t carry_count, void *workspace, size_t workspace_bytes,
                           void *stream) {
-  if (op != GA_OP_SUM) return fail(GA_ERR_UNSUPPORTED, "scan: only GA_OP_SUM is instantiated");
+  if (op < GA_OP_SUM || op > GA_OP_MIN) return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad op %d", (int)op);
   if (kind != GA_SCAN_INCLUSIVE && kind != GA_SCAN_EXCLUSIVE)
     return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad kind %d", (int)kind);
   if (!valid_dtype(dt)) return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad dtype %d", (int)dt);
-  if (dt != GA_I32 && dt != GA_I64) return fail(GA_ERR_UNSUPPORTED, "scan: dtype %d not instantiated", (int)dt);
   if (n < 0) return fail(GA_ERR_INVALID_ARGUMENT, "scan: n < 0");
   if (carry_count < 0 || (carry_count > 0 && !carry))
     return fail(GA_ERR_INVALID_ARGUMENT, "scan: carry_count < 0 or carry NULL");
@@ -137,7 +136,7 @@ ga_status_t gpuarray_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_
   if (partial_overlap(out, bytes, in, bytes)) return fail(GA_ERR_INVALID_ARGUMENT, "scan: out partially overlaps in");
   const size_t need = scan_workspace_bytes(dt, n);
   if (!workspace || workspace_bytes < need) return fail(GA_ERR_WORKSPACE, "scan: workspace needs %zu bytes", need);
-  return launch_scan(kind, dt, n, in, out, carry, carry_count, workspace, (cudaStream_t)stream);
+  return launch_scan(op, kind, dt, n, in, out, carry, carry_count, workspace, (cudaStream_t)stream);
 }
 
 const char *gpuarray_status_string(ga_status_t s) {

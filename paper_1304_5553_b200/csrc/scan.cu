@@ -1,6 +1,7 @@
 // scan.cu — parallel prefix sum (§3.2.6: "GPU-based
-// parallel prefix sums (also known as `parallel scan')"), reduction
-// expression "+" over int32 / int64 (wrapping, R4/R14).
+// parallel prefix sums (also known as `parallel scan')") with the scan
+// expressions "+", max, min (the reduction expressions of P:479-485) over
+// int32 / int64 (wrapping, R4/R14) and float / double (R22).
 //
 // One launch, decoupled look-back across super-tiles (BASELINE.json
 // north_star), HBM traffic 1 read + 1 write per element when the super-tiles
@@ -42,7 +43,7 @@ using namespace scan_detail;
 constexpr int L2_WARPS = 24, L2_ROWS = 32, L2_UNROLL = 8, L2_DEPTH = 8;
 // Fallback for arrays that are not 16-byte aligned: register tile of
 // 256 threads x 16 scalar-loaded items.
-constexpr int RG_BLOCK = 256, RG_ITEMS = 16;
+constexpr int RG_BLOCK = 256, RG_ITEMS = 16, RG_DEPTH = 4;
 
 template <typename T>
 constexpr int64_t l2_tile() {
@@ -56,7 +57,7 @@ size_t ws_bytes(int64_t n) {
   return HEADER + status_bytes<T>(cdiv(n, min_tile));
 }
 
-template <typename T, bool EXCLUSIVE>
+template <int OP, typename T, bool EXCLUSIVE>
 ga_status_t run(int64_t n, const void *in, void *out, const void *carry, int64_t carry_count, void *ws,
                 cudaStream_t s) {
   const bool aligned = ((uintptr_t)in & 15) == 0 && ((uintptr_t)out & 15) == 0;
@@ -65,18 +66,35 @@ ga_status_t run(int64_t n, const void *in, void *out, const void *carry, int64_t
     ScanArgs<T> p = make_args<T>(n, l2_tile<T>(), in, out, carry, carry_count, ws);
     const int grid = (int)p.num_tiles;
     if (inplace)
-      scan_l2_kernel<T, L2_WARPS, L2_ROWS, L2_UNROLL, L2_DEPTH, true, false, EXCLUSIVE, false, true>
+      scan_l2_kernel<OP, T, L2_WARPS, L2_ROWS, L2_UNROLL, L2_DEPTH, false, EXCLUSIVE, true>
           <<<grid, L2_WARPS * 32, 0, s>>>(p);
     else
-      scan_l2_kernel<T, L2_WARPS, L2_ROWS, L2_UNROLL, L2_DEPTH, true, true, EXCLUSIVE, false, true>
+      scan_l2_kernel<OP, T, L2_WARPS, L2_ROWS, L2_UNROLL, L2_DEPTH, true, EXCLUSIVE, true>
           <<<grid, L2_WARPS * 32, 0, s>>>(p);
   } else {
     ScanArgs<T> p = make_args<T>(n, (int64_t)RG_BLOCK * RG_ITEMS, in, out, carry, carry_count, ws);
     if (p.num_tiles > 0x7fffffffLL) return fail(GA_ERR_UNSUPPORTED, "scan: n too large (%lld)", (long long)n);
-    scan_kernel<T, RG_BLOCK, RG_ITEMS, 1, 0, EXCLUSIVE, false, false><<<(int)p.num_tiles, RG_BLOCK, 0, s>>>(p);
+    scan_reg_kernel<OP, T, RG_BLOCK, RG_ITEMS, RG_DEPTH, EXCLUSIVE><<<(int)p.num_tiles, RG_BLOCK, 0, s>>>(p);
   }
   count_launch();
   return check_launch("scan_kernel");
+}
+
+template <int OP, typename T>
+ga_status_t by_kind(bool ex, int64_t n, const void *in, void *out, const void *carry, int64_t cc, void *ws,
+                    cudaStream_t s) {
+  return ex ? run<OP, T, true>(n, in, out, carry, cc, ws, s) : run<OP, T, false>(n, in, out, carry, cc, ws, s);
+}
+
+template <typename T>
+ga_status_t by_op(ga_op_t op, bool ex, int64_t n, const void *in, void *out, const void *carry, int64_t cc, void *ws,
+                  cudaStream_t s) {
+  switch (op) {
+    case GA_OP_SUM: return by_kind<GA_OP_SUM, T>(ex, n, in, out, carry, cc, ws, s);
+    case GA_OP_MAX: return by_kind<GA_OP_MAX, T>(ex, n, in, out, carry, cc, ws, s);
+    case GA_OP_MIN: return by_kind<GA_OP_MIN, T>(ex, n, in, out, carry, cc, ws, s);
+  }
+  return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad op %d", (int)op);
 }
 
 }  // namespace
@@ -85,22 +103,22 @@ size_t scan_workspace_bytes(ga_dtype_t dt, int64_t n) {
   switch (dt) {
     case GA_I32: return ws_bytes<int32_t>(n);
     case GA_I64: return ws_bytes<int64_t>(n);
-    default: return 0;
+    case GA_F32: return ws_bytes<float>(n);
+    case GA_F64: return ws_bytes<double>(n);
   }
+  return 0;
 }
 
-ga_status_t launch_scan(ga_scan_kind_t kind, ga_dtype_t dt, int64_t n, const void *in, void *out,
+ga_status_t launch_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_t n, const void *in, void *out,
                         const void *carry, int64_t carry_count, void *ws, cudaStream_t s) {
   const bool ex = kind == GA_SCAN_EXCLUSIVE;
   switch (dt) {
-    case GA_I32:
-      return ex ? run<int32_t, true>(n, in, out, carry, carry_count, ws, s)
-                : run<int32_t, false>(n, in, out, carry, carry_count, ws, s);
-    case GA_I64:
-      return ex ? run<int64_t, true>(n, in, out, carry, carry_count, ws, s)
-                : run<int64_t, false>(n, in, out, carry, carry_count, ws, s);
-    default: return fail(GA_ERR_UNSUPPORTED, "scan dtype %d not instantiated", (int)dt);
+    case GA_I32: return by_op<int32_t>(op, ex, n, in, out, carry, carry_count, ws, s);
+    case GA_I64: return by_op<int64_t>(op, ex, n, in, out, carry, carry_count, ws, s);
+    case GA_F32: return by_op<float>(op, ex, n, in, out, carry, carry_count, ws, s);
+    case GA_F64: return by_op<double>(op, ex, n, in, out, carry, carry_count, ws, s);
   }
+  return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad dtype %d", (int)dt);
 }
 
 }  // namespace ga

@@ -161,9 +161,11 @@ def min(x, out=None):  # noqa: A001
 
 
 # --------------------------------------------------------------- scan
-def scan(x, exclusive=False, out=None, carry=None):
-    """Prefix sum (int32/int64, wrapping).  `carry` is an optional 1-D device
-    tensor whose elements are all added in front (a sharded scan's offset)."""
+def scan(x, exclusive=False, out=None, carry=None, op=SUM):
+    """Scan with reduction expression `op` (SUM / MAX / MIN) over int32,
+    int64 (wrapping), float32, float64 (PAPER.md:496-499).  `carry` is an
+    optional 1-D device tensor whose elements are all folded in front (a
+    sharded scan's offset)."""
     _check_array("x", x)
     if out is None:
         out = torch.empty_like(x)
@@ -181,7 +183,7 @@ def scan(x, exclusive=False, out=None, carry=None):
     nb = _abi.gpuarray_scan_workspace_bytes(dt, x.numel())
     w = workspace("scan", x.device, s, nb)
     kind = GA_SCAN_EXCLUSIVE if exclusive else GA_SCAN_INCLUSIVE
-    check(_abi.gpuarray_scan(SUM, kind, dt, x.numel(), _ptr(x), _ptr(out), cptr, ccount, w.data_ptr(), w.numel(), s))
+    check(_abi.gpuarray_scan(op, kind, dt, x.numel(), _ptr(x), _ptr(out), cptr, ccount, w.data_ptr(), w.numel(), s))
     return out
 
 

@@ -51,7 +51,8 @@ def test_workspace_sizes(abi):
     b = abi.gpuarray_scan_workspace_bytes(abi.GA_I64, 1 << 20)
     tiles = (1 << 20) // 4096  # status for the smaller (fallback) tile of 4096 elements
     assert b == 256 + tiles * 4 + tiles * 16
-    assert abi.gpuarray_scan_workspace_bytes(abi.GA_F32, 100) == 0   # not instantiated
+    assert abi.gpuarray_scan_workspace_bytes(abi.GA_F32, 100) == a * 0 + 256 + 8   # float scans too
+    assert abi.gpuarray_scan_workspace_bytes(abi.GA_F64, 4096) == 256 + 16 + 16
 
 
 def test_argument_validation_is_synchronous(abi):
@@ -76,8 +77,8 @@ def test_argument_validation_is_synchronous(abi):
     assert R(0, 0, 0, 0, 4, 4096, None, 64, None, ws, None) == abi.GA_ERR_WORKSPACE
     S = abi.gpuarray_scan
     sw = abi.gpuarray_scan_workspace_bytes(abi.GA_I32, 100)
-    assert S(abi.GA_OP_MAX, 0, abi.GA_I32, 100, 4096, 8192, None, 0, 64, sw, None) == abi.GA_ERR_UNSUPPORTED
-    assert S(0, 0, abi.GA_F32, 100, 4096, 8192, None, 0, 64, sw, None) == abi.GA_ERR_UNSUPPORTED
+    assert S(5, 0, abi.GA_I32, 100, 4096, 8192, None, 0, 64, sw, None) == E                    # bad op
+    assert S(0, 0, 9, 100, 4096, 8192, None, 0, 64, sw, None) == E                            # bad dtype
     assert S(0, 3, abi.GA_I32, 100, 4096, 8192, None, 0, 64, sw, None) == E                   # bad kind
     assert S(0, 0, abi.GA_I32, 100, 4096, 8192, None, 2, 64, sw, None) == E                   # carry NULL
     assert S(0, 0, abi.GA_I32, 100, 4096, 4100, None, 0, 64, sw, None) == E                   # partial overlap

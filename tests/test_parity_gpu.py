@@ -326,7 +326,9 @@ def test_scan_empty_and_errors():
     e = torch.empty(0, dtype=torch.int32, device=DEV)
     assert ga.scan(e).numel() == 0
     with pytest.raises(TypeError):
-        ga.scan(torch.ones(4, device=DEV))  # fp32 scan not instantiated
+        ga.scan(torch.ones(4, device=DEV, dtype=torch.float16))  # dtype not supported
+    with pytest.raises(ValueError):
+        G.scan(torch.ones(4, device=DEV), op=7)  # bad scan expression
 
 
 def test_launch_accounting():
@@ -336,3 +338,69 @@ def test_launch_accounting():
     ga.sum(x)
     ga.scan(torch.ones(1000, dtype=torch.int32, device=DEV))
     assert ga.launch_count() - c0 == 3
+
+
+# ------------------------------------------------------------------ scan breadth (NEXT-2)
+SCAN2_SIZES = [1, 33, 4097, 100_003, 1_000_003, (1 << 20) + 12345]
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.int64, np.float32, np.float64])
+@pytest.mark.parametrize("op", [oracle.MAX, oracle.MIN])
+@pytest.mark.parametrize("exclusive", [False, True])
+@pytest.mark.parametrize("n", SCAN2_SIZES)
+def test_scan_maxmin_bit_exact(dt, op, exclusive, n):
+    if np.dtype(dt).kind == "f":
+        x = host_data(dt, n, 6, signed=True)
+    else:
+        info = np.iinfo(dt)
+        x = np.random.default_rng(n).integers(info.min, info.max, size=n, dtype=dt, endpoint=True)
+    kind = oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE
+    for offs in (0, 1):  # aligned (super-tile kernel) and unaligned (register kernel)
+        got = G.scan(to_dev(x, offs), exclusive=exclusive, op=op).cpu().numpy()
+        assert_bit_exact(got, oracle.scan(kind, x, op=op))
+
+
+def test_scan_maxmin_nan_carry_inplace():
+    x = host_data(np.float32, 200_001, 7, signed=True)
+    x[[0, 5000, 199_999]] = np.nan
+    for op in (oracle.MAX, oracle.MIN):
+        for ex in (False, True):
+            c = np.array([0.5, -0.25], np.float32)
+            cv = np.float32(max(c) if op == oracle.MAX else min(c))
+            got = G.scan(to_dev(x), exclusive=ex, op=op, carry=to_dev(c)).cpu().numpy()
+            assert_bit_exact(got, oracle.scan(oracle.EXCLUSIVE if ex else oracle.INCLUSIVE, x, op=op, carry=cv))
+    xd = to_dev(x)
+    G.scan(xd, op=oracle.MAX, out=xd)
+    assert_bit_exact(xd.cpu().numpy(), oracle.scan(oracle.INCLUSIVE, x, op=oracle.MAX))
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("exclusive", [False, True])
+def test_scan_float_sum_small_integers_exact(dt, exclusive):
+    """Integer-valued floats whose prefix sums stay below 2^24 (fp32) are
+    summed exactly in any order: the float SUM scan must equal the integer
+    oracle bit for bit (catches a dropped, doubled or misplaced element)."""
+    n = 1_500_007  # 9 * n < 2^24
+    k = synth.host_fill(synth.I32_RANGE, 3, n, lo=0, hi=9)
+    x = k.astype(dt)
+    ref = oracle.scan(oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE, k).astype(dt)
+    for offs in (0, 3):
+        got = G.scan(to_dev(x, offs), exclusive=exclusive).cpu().numpy()
+        assert_bit_exact(got, ref)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("exclusive", [False, True])
+@pytest.mark.parametrize("n", [1, 4097, 1_000_003])
+def test_scan_float_sum_within_bound(dt, exclusive, n):
+    """Random signed data: |gpu_i - S_i| <= d_i * u * (|c| + sum_{j<=i}|x_j|)
+    with S_i the exact prefix sum and d_i = i/2048 + 512 (R22: the look-back
+    chains tile prefixes serially, the in-tile tree is shallow)."""
+    x = host_data(dt, n, 8, signed=True)
+    u = 2.0 ** -24 if dt == np.float32 else 2.0 ** -53
+    kind = oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE
+    ref, sa = oracle.scan(kind, x, return_sumabs=True)
+    for offs in (0, 1):
+        got = G.scan(to_dev(x, offs), exclusive=exclusive).cpu().numpy().astype(np.float64)
+        d = np.arange(n) / 2048.0 + 512
+        assert np.all(np.abs(got - ref) <= d * u * sa + 1e-300)

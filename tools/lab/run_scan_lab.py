@@ -15,7 +15,7 @@ def build():
     src = os.path.join(HERE, "scan_lab.cu")
     csrc = os.path.join(ROOT, "paper_1304_5553_b200", "csrc")
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-                           "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-shared", "-I", csrc,
+                           "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-shared", "-I", csrc, "-I", HERE,
                            "-I", os.path.join(ROOT, "include"), "-o", LIB, src])
 
 

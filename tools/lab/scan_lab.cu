@@ -4,9 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include "scan_kernel.cuh"
+#include "scan_variants.cuh"
 
-using namespace ga::scan_detail;
+using namespace ga::scan_lab_old;
 
 static unsigned long long *g_trace = nullptr;
 extern "C" void lab_set_trace(void *p) { g_trace = (unsigned long long *)p; }
