@@ -52,6 +52,9 @@ def parse():
     p.add_argument("--log2n", type=int, default=LOG2_N, help="per-GPU elements = 2^log2n (default 28)")
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--collective", choices=["nccl", "fused"], default="nccl",
+                   help="N>1: NCCL collectives via torch.distributed (default), or the fused in-kernel NVLink finish "
+                        "(gpuarray_reduce_xgpu over torch symmetric memory; validated on one GPU only so far)")
     return p.parse_args()
 
 
@@ -232,6 +235,10 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     ev = {op: [] for op in OPS}
+    xch = None
+    if world > 1 and args.collective == "fused":
+        xch = gdist.Exchange.symmetric(device=dev)
+        offset = torch.empty(1, dtype=torch.int32, device=dev)
 
     def step(record):
         def mark():
@@ -243,18 +250,28 @@ def main():
         e0 = mark()
         G.axpbyz(A, x, B, y, out=z)
         e1 = mark()
-        G.reduce(G.SUM, G.MUL, x, y, out=red[0:1])
-        e2 = mark()
-        G.reduce(G.SUM, G.ID, x, out=red[1:2])
-        e3 = mark()
-        G.reduce(G.SUM, G.SQUARE, x, out=red[2:3])
-        e4 = mark()
-        if world > 1:
-            dist.all_reduce(red, op=dist.ReduceOp.SUM)
-            gdist.scan(k, exclusive=True, out=s, totals=totals)
+        if xch is not None:  # fused: each reduction finishes across GPUs inside its own kernel
+            gdist.reduce_fused(G.SUM, G.MUL, x, y, out=red[0:1], exchange=xch)
+            e2 = mark()
+            gdist.reduce_fused(G.SUM, G.ID, x, out=red[1:2], exchange=xch)
+            e3 = mark()
+            gdist.reduce_fused(G.SUM, G.SQUARE, x, out=red[2:3], exchange=xch)
+            e4 = mark()
+            gdist.scan_fused(k, exclusive=True, out=s, exchange=xch, offset=offset)
+            e5 = mark()
         else:
-            G.scan(k, exclusive=True, out=s)
-        e5 = mark()
+            G.reduce(G.SUM, G.MUL, x, y, out=red[0:1])
+            e2 = mark()
+            G.reduce(G.SUM, G.ID, x, out=red[1:2])
+            e3 = mark()
+            G.reduce(G.SUM, G.SQUARE, x, out=red[2:3])
+            e4 = mark()
+            if world > 1:
+                dist.all_reduce(red, op=dist.ReduceOp.SUM)
+                gdist.scan(k, exclusive=True, out=s, totals=totals)
+            else:
+                G.scan(k, exclusive=True, out=s)
+            e5 = mark()
         if record:
             for op, (a, b) in zip(OPS, ((e0, e1), (e1, e2), (e2, e3), (e3, e4), (e4, e5))):
                 ev[op].append((a, b))
@@ -329,6 +346,8 @@ def main():
             "elements_per_s": round(world * n * len(OPS) / (ms_per_step * 1e-3), 1),
             "ops": ops, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "launches_per_step": launches / args.steps, "clocks": clk,
+            "collective": ("none (single GPU)" if world == 1 else
+                           "fused in-kernel NVLink finish" if xch is not None else "NCCL all_reduce + all_gather"),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

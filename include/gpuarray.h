@@ -116,6 +116,37 @@ ga_status_t gpuarray_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype
                             const void *x, const void *y, void *out, void *workspace,
                             size_t workspace_bytes, void *stream);
 
+/* ---- Fused cross-GPU finish (§8(a) a6 in one kernel).
+ * Bytes of the per-rank exchange buffer gpuarray_reduce_xgpu needs (2 x 64
+ * slots of 16 bytes).  Every rank allocates one in memory all ranks can
+ * address (torch symmetric memory over NVLink / NVSwitch), zero-filled once. */
+size_t gpuarray_xgpu_buffer_bytes(void);
+
+/* What the cross-GPU finish folds: every rank's result (a global reduction),
+ * or only the ranks before this one, in rank order (the exclusive prefix over
+ * ranks: a sharded scan's carry-in, §8(a) a7).  Rank 0's exclusive prefix is
+ * the neutral element. */
+typedef enum { GA_XGPU_ALL = 0, GA_XGPU_EXCLUSIVE_PREFIX = 1 } ga_xgpu_fold_t;
+
+/* gpuarray_reduce over a sharded array in ONE kernel per rank: the block that
+ * finishes the local reduction stores the local result into slot `rank` of
+ * every rank's exchange buffer (peer stores over NVLink, st.release.sys on a
+ * sequence word), waits until all `world` slots of its own buffer carry
+ * `seq`, and folds them (all, or only ranks < rank: see ga_xgpu_fold_t) in
+ * rank order into *out — so every rank ends with the same bits and no
+ * separate collective is launched.
+ *   peer_buffers  DEVICE array of `world` device pointers; [r] = rank r's
+ *                 exchange buffer as mapped on this device
+ *   rank, world   1 <= world <= 64
+ *   seq           call sequence number, >= 1, identical on all ranks for the
+ *                 same logical call and increasing by one per call
+ * Everything else as gpuarray_reduce.  All ranks must make the call (a rank
+ * that never arrives makes the others trap after 10 s instead of hanging). */
+ga_status_t gpuarray_reduce_xgpu(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
+                                 const void *x, const void *y, void *out, void *workspace, size_t workspace_bytes,
+                                 const uint64_t *peer_buffers, int rank, int world, uint64_t seq,
+                                 ga_xgpu_fold_t fold, void *stream);
+
 /* Bytes of workspace gpuarray_scan needs for (dt, n): a 256-byte header plus
  * per-tile look-back status.  Zero-fill once; reusable afterwards (status
  * words are epoch-tagged, the tile counter resets itself).  Never share it

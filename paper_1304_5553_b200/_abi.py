@@ -21,7 +21,7 @@ GA_OK, GA_ERR_INVALID_ARGUMENT, GA_ERR_UNSUPPORTED, GA_ERR_WORKSPACE, GA_ERR_CUD
 EXPORTS = (
     "gpuarray_axpbyz", "gpuarray_axpbz", "gpuarray_reduce_workspace_bytes", "gpuarray_reduce",
     "gpuarray_scan_workspace_bytes", "gpuarray_scan", "gpuarray_status_string", "gpuarray_last_error",
-    "gpuarray_abi_version", "gpuarray_launch_count",
+    "gpuarray_abi_version", "gpuarray_launch_count", "gpuarray_xgpu_buffer_bytes", "gpuarray_reduce_xgpu",
 )
 
 
@@ -62,7 +62,7 @@ def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
             f"{LIB_PATH} is missing: build the CUDA library first "
-            "(python -m paper_1304_5553_b200.build). There is no CPU fallback.")
+            "(python paper_1304_5553_b200/build.py). There is no CPU fallback.")
     lib = ctypes.CDLL(LIB_PATH)
     vp, i64, sz, st = ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t, ctypes.c_int
     lib.gpuarray_axpbyz.restype = st
@@ -85,6 +85,11 @@ def _load():
     lib.gpuarray_abi_version.argtypes = []
     lib.gpuarray_launch_count.restype = ctypes.c_uint64
     lib.gpuarray_launch_count.argtypes = []
+    lib.gpuarray_xgpu_buffer_bytes.restype = sz
+    lib.gpuarray_xgpu_buffer_bytes.argtypes = []
+    lib.gpuarray_reduce_xgpu.restype = st
+    lib.gpuarray_reduce_xgpu.argtypes = [st, st, st, st, i64, vp, vp, vp, vp, sz, vp, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_uint64, st, vp]
     return lib
 
 
@@ -109,6 +114,19 @@ def gpuarray_reduce_workspace_bytes(out_dt, n):
 
 def gpuarray_reduce(op, map_, in_dt, out_dt, n, x, y, out, workspace, workspace_bytes, stream):
     return LIB.gpuarray_reduce(op, map_, in_dt, out_dt, n, x, y, out, workspace, workspace_bytes, stream)
+
+
+def gpuarray_xgpu_buffer_bytes():
+    return LIB.gpuarray_xgpu_buffer_bytes()
+
+
+GA_XGPU_ALL, GA_XGPU_EXCLUSIVE_PREFIX = 0, 1
+
+
+def gpuarray_reduce_xgpu(op, map_, in_dt, out_dt, n, x, y, out, workspace, workspace_bytes, peer_buffers, rank, world,
+                         seq, fold, stream):
+    return LIB.gpuarray_reduce_xgpu(op, map_, in_dt, out_dt, n, x, y, out, workspace, workspace_bytes, peer_buffers,
+                                    rank, world, seq, fold, stream)
 
 
 def gpuarray_scan_workspace_bytes(dt, n):

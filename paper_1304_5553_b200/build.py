@@ -1,6 +1,10 @@
 """Compile the product library libgpuarray.so for sm_100a (nvcc, in-tree).
 
-    python -m paper_1304_5553_b200.build [--force]
+    python paper_1304_5553_b200/build.py [--force]
+
+Run as a file (or loaded by path, see __graft_entry__.py / tests/conftest.py):
+importing the package itself loads libgpuarray.so, which may be the stale
+library this script is about to replace.
 
 Only the product sources (csrc/*.cu + include/gpuarray.h) are compiled here.
 The CPU oracle and the synthetic generator have their own build steps

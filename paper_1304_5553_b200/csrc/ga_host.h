@@ -34,13 +34,25 @@ inline bool partial_overlap(const void *p, size_t bytes, const void *q, size_t b
   return a < b + bytes2 && b < a + bytes;
 }
 
+// Cross-GPU finish of a reduction (gpuarray_reduce_xgpu): device array of
+// `world` exchange-buffer pointers (one per rank, NVLink-mapped), own rank,
+// and the call's sequence number (identical on all ranks, >= 1).
+constexpr int XG_MAX_WORLD = 64;
+struct Exchange {
+  const unsigned long long *peers = nullptr;
+  int rank = 0;
+  int world = 0;
+  unsigned long long seq = 0;
+  int prefix_only = 0;  // 1: fold only ranks < rank (a sharded scan's offset)
+};
+
 // Launchers implemented per kernel family (elementwise.cu, reduce.cu, scan.cu).
 ga_status_t launch_axpbyz(ga_dtype_t dt, int64_t n, const ga_scalar_t &a, const void *x,
                           const ga_scalar_t &b, const void *y, void *z, cudaStream_t s);
 ga_status_t launch_axpbz(ga_dtype_t dt, int64_t n, const ga_scalar_t &a, const void *x,
                          const ga_scalar_t &b, void *z, cudaStream_t s);
 ga_status_t launch_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
-                          const void *x, const void *y, void *out, void *ws, cudaStream_t s);
+                          const void *x, const void *y, void *out, void *ws, const Exchange &xg, cudaStream_t s);
 ga_status_t launch_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_t n, const void *in, void *out,
                         const void *carry, int64_t carry_count, void *ws, cudaStream_t s);
 

@@ -114,7 +114,36 @@ ga_status_t gpuarray_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype
   if (map == GA_MAP_MUL && n > 0 && !y) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: MAP_MUL needs y");
   if (!workspace || workspace_bytes < reduce_workspace_bytes())
     return fail(GA_ERR_WORKSPACE, "reduce: workspace needs %zu bytes", reduce_workspace_bytes());
-  return launch_reduce(op, map, in_dt, out_dt, n, x, map == GA_MAP_MUL ? y : nullptr, out, workspace,
+  return launch_reduce(op, map, in_dt, out_dt, n, x, map == GA_MAP_MUL ? y : nullptr, out, workspace, Exchange(),
+                       (cudaStream_t)stream);
+}
+
+size_t gpuarray_xgpu_buffer_bytes(void) { return (size_t)2 * XG_MAX_WORLD * 16; }
+
+ga_status_t gpuarray_reduce_xgpu(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
+                                 const void *x, const void *y, void *out, void *workspace, size_t workspace_bytes,
+                                 const uint64_t *peer_buffers, int rank, int world, uint64_t seq,
+                                 ga_xgpu_fold_t fold, void *stream) {
+  if (op < GA_OP_SUM || op > GA_OP_MIN) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: bad op %d", (int)op);
+  if (map < GA_MAP_ID || map > GA_MAP_SQUARE) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: bad map");
+  if (!valid_dtype(in_dt) || !valid_dtype(out_dt)) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: bad dtype");
+  if (n < 0) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: n < 0");
+  if (!out) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: out is NULL");
+  if (n > 0 && !x) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: x is NULL with n > 0");
+  if (map == GA_MAP_MUL && n > 0 && !y) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: MAP_MUL needs y");
+  if (world < 1 || world > XG_MAX_WORLD || rank < 0 || rank >= world || !peer_buffers || seq == 0)
+    return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: bad rank/world/peers/seq");
+  if (fold != GA_XGPU_ALL && fold != GA_XGPU_EXCLUSIVE_PREFIX)
+    return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: bad fold %d", (int)fold);
+  if (!workspace || workspace_bytes < reduce_workspace_bytes())
+    return fail(GA_ERR_WORKSPACE, "reduce_xgpu: workspace needs %zu bytes", reduce_workspace_bytes());
+  Exchange xg;
+  xg.peers = reinterpret_cast<const unsigned long long *>(peer_buffers);
+  xg.rank = rank;
+  xg.world = world;
+  xg.seq = seq;
+  xg.prefix_only = fold == GA_XGPU_EXCLUSIVE_PREFIX;
+  return launch_reduce(op, map, in_dt, out_dt, n, x, map == GA_MAP_MUL ? y : nullptr, out, workspace, xg,
                        (cudaStream_t)stream);
 }
 

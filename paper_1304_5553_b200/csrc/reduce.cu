@@ -79,7 +79,54 @@ struct RedArgs {
   Tacc *out;
   Tacc *partials;
   unsigned int *ticket;
+  Exchange xg;  // cross-GPU finish (world == 0: none)
 };
+
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Cross-GPU finish (thread 0 of the last block), §8(f) NEXT-1: publish the
+// local result into slot `rank` of every rank's exchange buffer (peer
+// pointers: NVLink-mapped symmetric memory), then wait for all `world` slots
+// of the own buffer and fold them in rank order, so every rank computes the
+// same bits with no separate collective launch (prefix_only: the fold of the
+// ranks before this one — the offset of a sharded scan).  Slot entry = {value: 8 B,
+// seq: 8 B}; slots are double-buffered by seq parity (a rank cannot publish
+// call seq+2 before every rank has read call seq).
+template <int OP, typename Tacc>
+__device__ Tacc exchange_fold(const Exchange &xg, Tacc local) {
+  const int par = (int)(xg.seq & 1);
+  for (int r = 0; r < xg.world; ++r) {
+    char *e = reinterpret_cast<char *>(xg.peers[r]) + ((size_t)par * XG_MAX_WORLD + xg.rank) * 16;
+    *reinterpret_cast<Tacc *>(e) = local;
+    st_release_sys_u64(reinterpret_cast<unsigned long long *>(e + 8), xg.seq);
+  }
+  const char *own = reinterpret_cast<const char *>(xg.peers[xg.rank]);
+  Tacc v = Op<OP, Tacc>::neutral();
+  for (int r = 0; r < xg.world; ++r) {
+    const char *e = own + ((size_t)par * XG_MAX_WORLD + r) * 16;
+    const unsigned long long *f = reinterpret_cast<const unsigned long long *>(e + 8);
+    uint32_t spins = 0;
+    uint64_t t0 = 0;
+    while (ld_acquire_sys_u64(f) != xg.seq) {
+      if ((++spins & 1023u) == 0) {
+        uint64_t now;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 10000000000ull) __trap();  // a rank never arrived
+      }
+    }
+    // every rank is waited for (slot-reuse safety); prefix_only folds r < rank
+    if (!xg.prefix_only || r < xg.rank) v = Op<OP, Tacc>::fold(v, *reinterpret_cast<const volatile Tacc *>(e));
+  }
+  return v;
+}
 
 // Block-wide fold; result valid in thread 0.  Fixed order.
 template <int OP, typename T>
@@ -173,8 +220,9 @@ __global__ void __launch_bounds__(RED_BLOCK) reduce_kernel(RedArgs<Tin, Tacc> p)
   __syncthreads();  // smem reuse
   w = block_fold<OP, Tacc>(w, smem);
   if (threadIdx.x == 0) {
-    *p.out = w;
     *p.ticket = 0u;  // reusable by the next call on this workspace
+    if (p.xg.world > 0) w = exchange_fold<OP, Tacc>(p.xg, w);
+    *p.out = w;
   }
 }
 
@@ -184,8 +232,8 @@ __global__ void neutral_kernel(Tacc *out) {
 }
 
 template <typename Tin, typename Tacc, int OP, int MAP>
-ga_status_t run(int64_t n, const void *x, const void *y, void *out, void *ws, cudaStream_t s) {
-  if (n == 0) {
+ga_status_t run(int64_t n, const void *x, const void *y, void *out, void *ws, const Exchange &xg, cudaStream_t s) {
+  if (n == 0 && xg.world == 0) {
     neutral_kernel<Tacc, OP><<<1, 1, 0, s>>>(static_cast<Tacc *>(out));
     count_launch();
     return check_launch("neutral_kernel");
@@ -199,6 +247,7 @@ ga_status_t run(int64_t n, const void *x, const void *y, void *out, void *ws, cu
   p.out = static_cast<Tacc *>(out);
   p.ticket = static_cast<unsigned int *>(ws);
   p.partials = reinterpret_cast<Tacc *>(static_cast<char *>(ws) + RED_HEADER);
+  p.xg = xg;
 
   const uintptr_t phase = (uintptr_t)x & 31;
   const bool coaligned = (MAP != GA_MAP_MUL || ((uintptr_t)y & 31) == phase) && (phase % sizeof(Tin)) == 0;
@@ -213,25 +262,27 @@ ga_status_t run(int64_t n, const void *x, const void *y, void *out, void *ws, cu
   // one CTA per chunk of RED_BLOCK*UNROLL vectors (or RED_BLOCK scalars on
   // the unaligned path), capped at RED_MAX_PARTIALS
   const int64_t units = coaligned ? cdiv(std::max<int64_t>(p.nvec, 1), (int64_t)RED_BLOCK * UNROLL) : cdiv(n, RED_BLOCK);
-  const int grid = (int)std::min<int64_t>(units, RED_MAX_PARTIALS);
+  const int grid = (int)std::max<int64_t>(std::min<int64_t>(units, RED_MAX_PARTIALS), 1);
   kern<<<grid, RED_BLOCK, 0, s>>>(p);
   count_launch();
   return check_launch("reduce_kernel");
 }
 
 template <typename Tin, typename Tacc, int OP>
-ga_status_t by_map(ga_map_t map, int64_t n, const void *x, const void *y, void *out, void *ws, cudaStream_t s) {
+ga_status_t by_map(ga_map_t map, int64_t n, const void *x, const void *y, void *out, void *ws, const Exchange &xg,
+                   cudaStream_t s) {
   switch (map) {
-    case GA_MAP_ID: return run<Tin, Tacc, OP, GA_MAP_ID>(n, x, y, out, ws, s);
-    case GA_MAP_MUL: return run<Tin, Tacc, OP, GA_MAP_MUL>(n, x, y, out, ws, s);
-    case GA_MAP_SQUARE: return run<Tin, Tacc, OP, GA_MAP_SQUARE>(n, x, y, out, ws, s);
+    case GA_MAP_ID: return run<Tin, Tacc, OP, GA_MAP_ID>(n, x, y, out, ws, xg, s);
+    case GA_MAP_MUL: return run<Tin, Tacc, OP, GA_MAP_MUL>(n, x, y, out, ws, xg, s);
+    case GA_MAP_SQUARE: return run<Tin, Tacc, OP, GA_MAP_SQUARE>(n, x, y, out, ws, xg, s);
   }
   return fail(GA_ERR_INVALID_ARGUMENT, "bad map %d", (int)map);
 }
 
 template <typename T, int OP>
-ga_status_t maxmin(ga_map_t map, int64_t n, const void *x, const void *y, void *out, void *ws, cudaStream_t s) {
-  return by_map<T, T, OP>(map, n, x, y, out, ws, s);
+ga_status_t maxmin(ga_map_t map, int64_t n, const void *x, const void *y, void *out, void *ws, const Exchange &xg,
+                   cudaStream_t s) {
+  return by_map<T, T, OP>(map, n, x, y, out, ws, xg, s);
 }
 
 }  // namespace
@@ -239,30 +290,30 @@ ga_status_t maxmin(ga_map_t map, int64_t n, const void *x, const void *y, void *
 size_t reduce_workspace_bytes() { return RED_HEADER + (size_t)RED_MAX_PARTIALS * 8; }
 
 ga_status_t launch_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
-                          const void *x, const void *y, void *out, void *ws, cudaStream_t s) {
+                          const void *x, const void *y, void *out, void *ws, const Exchange &xg, cudaStream_t s) {
   if (op == GA_OP_SUM) {
-    if (in_dt == GA_F32 && out_dt == GA_F32) return by_map<float, float, GA_OP_SUM>(map, n, x, y, out, ws, s);
-    if (in_dt == GA_F32 && out_dt == GA_F64) return by_map<float, double, GA_OP_SUM>(map, n, x, y, out, ws, s);
-    if (in_dt == GA_F64 && out_dt == GA_F64) return by_map<double, double, GA_OP_SUM>(map, n, x, y, out, ws, s);
-    if (in_dt == GA_I32 && out_dt == GA_I32) return by_map<int32_t, int32_t, GA_OP_SUM>(map, n, x, y, out, ws, s);
-    if (in_dt == GA_I32 && out_dt == GA_I64) return by_map<int32_t, int64_t, GA_OP_SUM>(map, n, x, y, out, ws, s);
-    if (in_dt == GA_I64 && out_dt == GA_I64) return by_map<int64_t, int64_t, GA_OP_SUM>(map, n, x, y, out, ws, s);
+    if (in_dt == GA_F32 && out_dt == GA_F32) return by_map<float, float, GA_OP_SUM>(map, n, x, y, out, ws, xg, s);
+    if (in_dt == GA_F32 && out_dt == GA_F64) return by_map<float, double, GA_OP_SUM>(map, n, x, y, out, ws, xg, s);
+    if (in_dt == GA_F64 && out_dt == GA_F64) return by_map<double, double, GA_OP_SUM>(map, n, x, y, out, ws, xg, s);
+    if (in_dt == GA_I32 && out_dt == GA_I32) return by_map<int32_t, int32_t, GA_OP_SUM>(map, n, x, y, out, ws, xg, s);
+    if (in_dt == GA_I32 && out_dt == GA_I64) return by_map<int32_t, int64_t, GA_OP_SUM>(map, n, x, y, out, ws, xg, s);
+    if (in_dt == GA_I64 && out_dt == GA_I64) return by_map<int64_t, int64_t, GA_OP_SUM>(map, n, x, y, out, ws, xg, s);
     return fail(GA_ERR_UNSUPPORTED, "SUM %d -> %d not instantiated", (int)in_dt, (int)out_dt);
   }
   if (in_dt != out_dt) return fail(GA_ERR_UNSUPPORTED, "MAX/MIN need out_dt == in_dt");
   if (op == GA_OP_MAX) {
     switch (in_dt) {
-      case GA_F32: return maxmin<float, GA_OP_MAX>(map, n, x, y, out, ws, s);
-      case GA_F64: return maxmin<double, GA_OP_MAX>(map, n, x, y, out, ws, s);
-      case GA_I32: return maxmin<int32_t, GA_OP_MAX>(map, n, x, y, out, ws, s);
-      case GA_I64: return maxmin<int64_t, GA_OP_MAX>(map, n, x, y, out, ws, s);
+      case GA_F32: return maxmin<float, GA_OP_MAX>(map, n, x, y, out, ws, xg, s);
+      case GA_F64: return maxmin<double, GA_OP_MAX>(map, n, x, y, out, ws, xg, s);
+      case GA_I32: return maxmin<int32_t, GA_OP_MAX>(map, n, x, y, out, ws, xg, s);
+      case GA_I64: return maxmin<int64_t, GA_OP_MAX>(map, n, x, y, out, ws, xg, s);
     }
   } else if (op == GA_OP_MIN) {
     switch (in_dt) {
-      case GA_F32: return maxmin<float, GA_OP_MIN>(map, n, x, y, out, ws, s);
-      case GA_F64: return maxmin<double, GA_OP_MIN>(map, n, x, y, out, ws, s);
-      case GA_I32: return maxmin<int32_t, GA_OP_MIN>(map, n, x, y, out, ws, s);
-      case GA_I64: return maxmin<int64_t, GA_OP_MIN>(map, n, x, y, out, ws, s);
+      case GA_F32: return maxmin<float, GA_OP_MIN>(map, n, x, y, out, ws, xg, s);
+      case GA_F64: return maxmin<double, GA_OP_MIN>(map, n, x, y, out, ws, xg, s);
+      case GA_I32: return maxmin<int32_t, GA_OP_MIN>(map, n, x, y, out, ws, xg, s);
+      case GA_I64: return maxmin<int64_t, GA_OP_MIN>(map, n, x, y, out, ws, xg, s);
     }
   }
   return fail(GA_ERR_INVALID_ARGUMENT, "bad op %d", (int)op);

@@ -89,3 +89,78 @@ def scan(x, exclusive=False, out=None, group=None, ops=None, totals=None):
     dist.all_gather_into_tensor(gathered, mine, group=group)
     carry = gathered[:rank] if rank > 0 else None
     return ops.scan(x, exclusive=exclusive, out=out, carry=carry)
+
+
+# ---------------------------------------------------------------- fused cross-GPU finish (NEXT-1)
+class Exchange:
+    """Exchange buffers for gpuarray_reduce_xgpu: `peers` is a device array
+    of every rank's buffer address as seen from this rank, `rank`/`world`
+    this rank's place, `seq` the per-call sequence number (identical on all
+    ranks because every rank makes the same calls in the same order)."""
+
+    def __init__(self, peers, rank, world, keepalive=None):
+        self.peers = peers
+        self.rank = rank
+        self.world = world
+        self.seq = 0
+        self._keepalive = keepalive
+
+    def next_seq(self):
+        self.seq += 1
+        return self.seq
+
+    @classmethod
+    def symmetric(cls, group=None, device=None):
+        """Buffers in torch symmetric memory (NVLink-mapped on every peer)."""
+        from torch.distributed import _symmetric_memory as symm_mem
+
+        from . import _abi
+        device = device or torch.device("cuda", torch.cuda.current_device())
+        nbytes = _abi.gpuarray_xgpu_buffer_bytes()
+        buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+        buf.zero_()
+        group = group or dist.group.WORLD
+        hdl = symm_mem.rendezvous(buf, group)
+        peers = torch.tensor([int(p) for p in hdl.buffer_ptrs], dtype=torch.int64, device=device)
+        torch.cuda.synchronize(device)
+        dist.barrier(group)
+        return cls(peers, hdl.rank, hdl.world_size, keepalive=(buf, hdl))
+
+
+def reduce_fused(op, map_, x, y=None, out_dtype=None, out=None, exchange=None, prefix_only=False):
+    """Global map-reduce of a sharded array in ONE kernel per rank: the
+    local reduction's last block publishes its result to every rank over
+    NVLink and folds all ranks' results in rank order (include/gpuarray.h,
+    gpuarray_reduce_xgpu)."""
+    from . import _abi
+    from . import gpuarray as G
+    G._check_array("x", x)
+    if map_ == G.MUL:
+        if y is None:
+            raise ValueError("map MUL needs y")
+        G._same(x, y, "y")
+    out_dtype = x.dtype if out_dtype is None else out_dtype
+    if out is None:
+        out = torch.empty((), dtype=out_dtype, device=x.device)
+    in_dt, out_dt = G.ga_dtype(x.dtype), G.ga_dtype(out_dtype)
+    s = G._stream(x)
+    nb = _abi.gpuarray_reduce_workspace_bytes(out_dt, x.numel())
+    w = G.workspace("reduce", x.device, s, nb)
+    seq = exchange.next_seq()
+    G.check(_abi.gpuarray_reduce_xgpu(op, map_, in_dt, out_dt, x.numel(), G._ptr(x),
+                                      G._ptr(y) if map_ == G.MUL else None, out.data_ptr(), w.data_ptr(), w.numel(),
+                                      exchange.peers.data_ptr(), exchange.rank, exchange.world, seq,
+                                      _abi.GA_XGPU_EXCLUSIVE_PREFIX if prefix_only else _abi.GA_XGPU_ALL, s))
+    return out
+
+
+def scan_fused(x, exclusive=False, out=None, exchange=None, offset=None):
+    """Global prefix sum of a sharded integer array with no collective
+    launch: the local reduce kernel's fused finish returns the fold of the
+    totals of ranks < rank (the shard's offset, on the device), which the
+    local scan takes as its carry-in."""
+    from . import gpuarray as G
+    if offset is None or offset.numel() != 1 or offset.dtype != x.dtype:
+        offset = torch.empty(1, dtype=x.dtype, device=x.device)
+    reduce_fused(G.SUM, G.ID, x, out_dtype=x.dtype, out=offset, exchange=exchange, prefix_only=True)
+    return G.scan(x, exclusive=exclusive, out=out, carry=offset)

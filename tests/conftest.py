@@ -23,3 +23,13 @@ def golden():
         with open(os.path.join(GOLDEN, name)) as f:
             return json.load(f)
     return load
+
+
+def product_build():
+    """Build libgpuarray.so if stale, without importing the package first."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("ga_product_build",
+                                                  os.path.join(ROOT, "paper_1304_5553_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.build()

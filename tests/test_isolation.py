@@ -46,8 +46,8 @@ def test_importing_product_does_not_load_oracle():
 def test_product_library_does_not_link_oracle():
     lib = os.path.join(PKG, "libgpuarray.so")
     if not os.path.exists(lib):
-        from paper_1304_5553_b200 import build
-        build.build()
+        from conftest import product_build
+        product_build()
     deps = subprocess.run(["ldd", lib], capture_output=True, text=True).stdout
     assert "oracle" not in deps
     syms = subprocess.run(["nm", "-D", lib], capture_output=True, text=True).stdout

@@ -16,8 +16,8 @@ LIB = os.path.join(ROOT, "paper_1304_5553_b200", "libgpuarray.so")
 
 @pytest.fixture(scope="module")
 def sass():
-    from paper_1304_5553_b200 import build
-    build.build()
+    from conftest import product_build
+    product_build()
     out = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
     funcs = {}
     cur = None
