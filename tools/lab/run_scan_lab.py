@@ -8,11 +8,12 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
-LIB = os.path.join(HERE, "libscan_lab.so")
+LIB = os.path.join(HERE, os.environ.get("SCAN_LAB_LIB", "libscan_lab.so"))
+SRC = os.environ.get("SCAN_LAB_SRC", "scan_lab.cu")
 
 
 def build():
-    src = os.path.join(HERE, "scan_lab.cu")
+    src = os.path.join(HERE, SRC)
     csrc = os.path.join(ROOT, "paper_1304_5553_b200", "csrc")
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
                            "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-shared", "-I", csrc, "-I", HERE,
@@ -25,6 +26,7 @@ def main():
     from paper_1304_5553_b200 import gpuarray as G
     lg = int(sys.argv[1]) if len(sys.argv) > 1 else 28
     only = [int(a) for a in sys.argv[2:]]
+    variants = [int(v) for v in os.environ["SCAN_LAB_VARIANTS"].split(",")] if "SCAN_LAB_VARIANTS" in os.environ else None
     if not os.path.exists(LIB):
         build()
     L = ctypes.CDLL(LIB)
@@ -41,7 +43,7 @@ def main():
     ws = torch.zeros(256 + 32 * n // 64 + (1 << 20), dtype=torch.uint8, device=dev)
     s = torch.cuda.current_stream().cuda_stream
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for v in [142, 232, 161] + list(range(240, 250)):
+    for v in variants or [142, 232, 161] + list(range(240, 250)):
         if only and v not in only:
             continue
         is64 = L.lab_scan_elem_bytes(v) == 8
