@@ -1,0 +1,236 @@
+// reduce_kernel.cuh — the single-pass map-reduce kernel (see reduce.cu for
+// the algorithm and its citations), templated on its CTA shape so reduce.cu
+// instantiates the tuned one and tools/lab can time others.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "ga_device.cuh"
+#include "ga_host.h"
+
+namespace ga {
+namespace red_detail {
+
+
+constexpr int RED_MAX_PARTIALS = 32768;
+constexpr size_t RED_HEADER = 128;  // ticket lives in its own 128-byte line
+
+template <typename T>
+__host__ __device__ constexpr bool is_fp() {
+  return std::is_floating_point<T>::value;
+}
+
+// Map (over index i) then accumulate into the reduction's accumulator.
+// SUM over floats accumulates in Tacc with one fused multiply-add per term
+// (exact product, one rounding): the tolerance of DESIGN.md R9/R10 applies.
+// SUM over integers widens to Tacc, then wraps (R3, R4).  MAX/MIN evaluate
+// the map in Tin with RN / wrap (R3) and fold with maxNum/minNum (R6).
+template <typename Tin, typename Tacc, int OP, int MAP>
+__device__ __forceinline__ Tacc map_acc(Tacc acc, Tin x, Tin y) {
+  if constexpr (OP == GA_OP_SUM) {
+    const Tacc u = (Tacc)x;
+    if constexpr (is_fp<Tacc>()) {
+      if constexpr (MAP == GA_MAP_ID) return e_add(acc, u);
+      else if constexpr (MAP == GA_MAP_MUL) return e_fma(u, (Tacc)y, acc);
+      else return e_fma(u, u, acc);
+    } else {
+      if constexpr (MAP == GA_MAP_ID) return e_add(acc, u);
+      else if constexpr (MAP == GA_MAP_MUL) return e_add(acc, e_mul(u, (Tacc)y));
+      else return e_add(acc, e_mul(u, u));
+    }
+  } else {
+    Tin t;
+    if constexpr (MAP == GA_MAP_ID) t = x;
+    else if constexpr (MAP == GA_MAP_MUL) t = e_mul(x, y);
+    else t = e_mul(x, x);
+    return Op<OP, Tacc>::fold(acc, (Tacc)t);
+  }
+}
+
+template <typename Tin, typename Tacc>
+struct RedArgs {
+  int64_t n;
+  int64_t head;  // elements folded by the scalar loop before the aligned body
+  int64_t nvec;  // 32-byte vectors in the body
+  const Tin *x;
+  const Tin *y;
+  Tacc *out;
+  Tacc *partials;
+  unsigned int *ticket;
+  Exchange xg;  // cross-GPU finish (world == 0: none)
+};
+
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Cross-GPU finish (thread 0 of the last block), §8(f) NEXT-1: publish the
+// local result into slot `rank` of every rank's exchange buffer (peer
+// pointers: NVLink-mapped symmetric memory), then wait for all `world` slots
+// of the own buffer and fold them in rank order, so every rank computes the
+// same bits with no separate collective launch (prefix_only: the fold of the
+// ranks before this one — the offset of a sharded scan).  Slot entry = {value: 8 B,
+// seq: 8 B}; slots are double-buffered by seq parity (a rank cannot publish
+// call seq+2 before every rank has read call seq).
+template <int OP, typename Tacc>
+__device__ Tacc exchange_fold(const Exchange &xg, Tacc local) {
+  const int par = (int)(xg.seq & 1);
+  for (int r = 0; r < xg.world; ++r) {
+    char *e = reinterpret_cast<char *>(xg.peers[r]) + ((size_t)par * XG_MAX_WORLD + xg.rank) * 16;
+    *reinterpret_cast<Tacc *>(e) = local;
+    st_release_sys_u64(reinterpret_cast<unsigned long long *>(e + 8), xg.seq);
+  }
+  const char *own = reinterpret_cast<const char *>(xg.peers[xg.rank]);
+  Tacc v = Op<OP, Tacc>::neutral();
+  for (int r = 0; r < xg.world; ++r) {
+    const char *e = own + ((size_t)par * XG_MAX_WORLD + r) * 16;
+    const unsigned long long *f = reinterpret_cast<const unsigned long long *>(e + 8);
+    uint32_t spins = 0;
+    uint64_t t0 = 0;
+    while (ld_acquire_sys_u64(f) != xg.seq) {
+      if ((++spins & 1023u) == 0) {
+        uint64_t now;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 10000000000ull) __trap();  // a rank never arrived
+      }
+    }
+    // every rank is waited for (slot-reuse safety); prefix_only folds r < rank
+    if (!xg.prefix_only || r < xg.rank) v = Op<OP, Tacc>::fold(v, *reinterpret_cast<const volatile Tacc *>(e));
+  }
+  return v;
+}
+
+// Block-wide fold; result valid in thread 0.  Fixed order.
+template <int OP, int BLOCK, typename T>
+__device__ __forceinline__ T block_fold(T v, T *smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_fold<OP, T>(v);
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < BLOCK / 32 ? smem[lane] : Op<OP, T>::neutral();
+    v = warp_fold<OP, T>(v);
+  }
+  return v;
+}
+
+template <typename Tin, typename Tacc, int OP, int MAP, int UNROLL, int RED_BLOCK, int MINB>
+__global__ void __launch_bounds__(RED_BLOCK, MINB) reduce_kernel(RedArgs<Tin, Tacc> p) {
+  constexpr int VEC = 32 / sizeof(Tin);
+  constexpr bool HAS_Y = MAP == GA_MAP_MUL;
+  __shared__ Tacc smem[RED_BLOCK / 32];
+  __shared__ bool is_last;
+
+  const int64_t tid = (int64_t)blockIdx.x * RED_BLOCK + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * RED_BLOCK;
+
+  Tacc acc[VEC];
+#pragma unroll
+  for (int k = 0; k < VEC; ++k) acc[k] = Op<OP, Tacc>::neutral();
+
+  // Scalar parts: the unaligned head (all of x when x/y are not co-aligned)
+  // and the tail after the last whole vector.
+  for (int64_t i = tid; i < p.head; i += nthreads)
+    acc[0] = map_acc<Tin, Tacc, OP, MAP>(acc[0], p.x[i], HAS_Y ? p.y[i] : Tin(0));
+  const int64_t tail0 = p.head + p.nvec * VEC;
+  for (int64_t i = tail0 + tid; i < p.n; i += nthreads)
+    acc[VEC - 1] = map_acc<Tin, Tacc, OP, MAP>(acc[VEC - 1], p.x[i], HAS_Y ? p.y[i] : Tin(0));
+
+  const char *xb = reinterpret_cast<const char *>(p.x + p.head);
+  const char *yb = HAS_Y ? reinterpret_cast<const char *>(p.y + p.head) : nullptr;
+  constexpr int64_t CHUNK = (int64_t)RED_BLOCK * UNROLL;
+  // Out-of-range vectors are filled with an input whose mapped value is the
+  // neutral element (0 for SUM under any map; the neutral itself for MAX/MIN
+  // under the identity map), so the accumulation is unconditional.  MAX/MIN
+  // under x*y or x*x have no such input and keep the guard.
+  constexpr bool FILL = OP == GA_OP_SUM || MAP == GA_MAP_ID;
+  V32 fill;
+#pragma unroll
+  for (int k = 0; k < VEC; ++k) vset<Tin>(fill, k, OP == GA_OP_SUM ? Tin(0) : (Tin)Op<OP, Tacc>::neutral());
+  // One batch: UNROLL vectors per input, RED_BLOCK apart, all loaded before
+  // any is used; out-of-range vectors take the neutral fill.
+  auto batch = [&](int64_t base) {
+    V32 vx[UNROLL], vy[UNROLL];
+#pragma unroll
+    for (int j = 0; j < UNROLL; ++j) {
+      const int64_t v = base + j * RED_BLOCK;
+      if (v < p.nvec) {
+        vx[j] = ld_nc_256(xb + v * 32);
+        if constexpr (HAS_Y) vy[j] = ld_nc_256(yb + v * 32);
+      } else {
+        vx[j] = fill;
+        vy[j] = fill;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < UNROLL; ++j)
+      if (FILL || base + j * RED_BLOCK < p.nvec) {
+#pragma unroll
+        for (int k = 0; k < VEC; ++k)
+          acc[k] = map_acc<Tin, Tacc, OP, MAP>(acc[k], vget<Tin>(vx[j], k), HAS_Y ? vget<Tin>(vy[j], k) : Tin(0));
+      }
+  };
+  // The first batch is peeled out of the loop (the loop only runs when the
+  // grid was capped): ptxas then schedules it like straight-line code — all
+  // loads first — instead of squeezing the loop body into 32 registers.
+  const int64_t base0 = (int64_t)blockIdx.x * CHUNK + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * CHUNK;
+  if (base0 < p.nvec) batch(base0);
+#pragma unroll 1
+  for (int64_t base = base0 + stride; base < p.nvec; base += stride) batch(base);
+
+  // Lane tree: ((a0+a4)+(a2+a6)) + ((a1+a5)+(a3+a7)) for VEC = 8.
+#pragma unroll
+  for (int w = VEC / 2; w >= 1; w >>= 1) {
+#pragma unroll
+    for (int k = 0; k < w; ++k) acc[k] = Op<OP, Tacc>::fold(acc[k], acc[k + w]);
+  }
+  Tacc v = block_fold<OP, RED_BLOCK, Tacc>(acc[0], smem);
+
+  if (threadIdx.x == 0) {
+    p.partials[blockIdx.x] = v;
+    __threadfence();
+    is_last = atomicAdd(p.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!is_last) return;
+
+  // Last block: fold the partials in index order (L2 reads, bypassing L1).
+  __threadfence();
+  // 8 independent L2 loads per thread in flight (a dependent one-by-one loop
+  // over up to 64 partials per thread cost several microseconds of tail).
+  Tacc w = Op<OP, Tacc>::neutral();
+  for (int base = threadIdx.x; base < (int)gridDim.x; base += RED_BLOCK * 8) {
+    Tacc v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = base + j * RED_BLOCK;
+      v[j] = i < (int)gridDim.x ? __ldcg(p.partials + i) : Op<OP, Tacc>::neutral();
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) w = Op<OP, Tacc>::fold(w, v[j]);
+  }
+  __syncthreads();  // smem reuse
+  w = block_fold<OP, RED_BLOCK, Tacc>(w, smem);
+  if (threadIdx.x == 0) {
+    *p.ticket = 0u;  // reusable by the next call on this workspace
+    if (p.xg.world > 0) w = exchange_fold<OP, Tacc>(p.xg, w);
+    *p.out = w;
+  }
+}
+
+template <typename Tacc, int OP>
+__global__ void neutral_kernel(Tacc *out) {
+  *out = Op<OP, Tacc>::neutral();
+}
+
+}  // namespace red_detail
+}  // namespace ga

@@ -3,14 +3,15 @@ import ctypes, os, subprocess, sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
-LIB = os.path.join(HERE, "libred_lab.so")
+LIB = os.path.join(HERE, os.environ.get("RED_LAB_LIB", "libred_lab.so"))
+SRC = os.environ.get("RED_LAB_SRC", "red_lab.cu")
 
 
 def build():
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
                            "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-shared",
                            "-I", os.path.join(ROOT, "paper_1304_5553_b200", "csrc"), "-I", os.path.join(ROOT, "include"),
-                           "-o", LIB, os.path.join(HERE, "red_lab.cu")])
+                           "-o", LIB, os.path.join(HERE, SRC)])
 
 
 def main():
@@ -36,6 +37,12 @@ def main():
     ms = t(lambda: G.sum(x, out=out)); print(f"product sum {ms*1e3:7.1f} us {4*n/ms/1e6:7.1f} GB/s")
     ms = t(lambda: G.dot(x, y, out=out)); print(f"product dot {ms*1e3:7.1f} us {8*n/ms/1e6:7.1f} GB/s")
     ms = t(lambda: torch.sum(x)); print(f"torch sum   {ms*1e3:7.1f} us {4*n/ms/1e6:7.1f} GB/s")
+    from paper_1304_5553_b200 import _abi
+    wsr = G.workspace("reduce", x.device, s, _abi.gpuarray_reduce_workspace_bytes(0, n))
+    args = (0, 0, 0, 0, n, x.data_ptr(), None, out.data_ptr(), wsr.data_ptr(), wsr.numel(), s)
+    ms = t(lambda: _abi.LIB.gpuarray_reduce(*args)); print(f"raw-abi sum {ms*1e3:7.1f} us {4*n/ms/1e6:7.1f} GB/s")
+    args = (0, 1, 0, 0, n, x.data_ptr(), y.data_ptr(), out.data_ptr(), wsr.data_ptr(), wsr.numel(), s)
+    ms = t(lambda: _abi.LIB.gpuarray_reduce(*args)); print(f"raw-abi dot {ms*1e3:7.1f} us {8*n/ms/1e6:7.1f} GB/s")
     # step context: an axpbyz on other arrays right before each timed reduce
     z1 = torch.empty_like(x); x2 = torch.empty_like(x).fill_(1.0); y2 = torch.empty_like(x).fill_(2.0)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
@@ -54,8 +61,8 @@ def main():
         b = 8 if v in (11, 21) else 4
         ms = ctx(lambda: L.red_lab(v, n, x.data_ptr(), y.data_ptr(), out.data_ptr(), ws.data_ptr(), s))
         print(f"ctx variant {v} {ms*1e3:7.1f} us {b*n/ms/1e6:7.1f} GB/s", flush=True)
-    for v in [0, 1, 2, 3, 4, 10, 11, 12, 13, 14, 20, 21]:
-        dot = v in (10, 11, 12, 13, 14, 21)
+    for v in ([int(q) for q in os.environ['RED_LAB_VARIANTS'].split(',')] if 'RED_LAB_VARIANTS' in os.environ else [1, 11]):
+        dot = v in (10, 11, 12, 13, 14, 15, 16, 17, 21, 34, 35)
         L.red_lab(v, n, x.data_ptr(), y.data_ptr(), out.data_ptr(), ws.data_ptr(), s)
         torch.cuda.synchronize()
         val = float(out[0])
