@@ -75,6 +75,13 @@ def lib():
         L.oracle_scan_maxmin_f64.argtypes = [ctypes.c_int, ctypes.c_int, i64, vp, vp, d]
         L.oracle_scan_maxmin_int.restype = None
         L.oracle_scan_maxmin_int.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, i64, vp, vp, i64]
+        for nm in ("oracle_axpbyz_c64", "oracle_axpbyz_c128"):
+            getattr(L, nm).restype = None
+            getattr(L, nm).argtypes = [i64, vp, vp, vp, vp, vp]
+        L.oracle_sum_complex.restype = None
+        L.oracle_sum_complex.argtypes = [ctypes.c_int, ctypes.c_int, i64, vp, vp, vp, vp]
+        L.oracle_norm2_complex.restype = d
+        L.oracle_norm2_complex.argtypes = [ctypes.c_int, i64, vp]
         L.oracle_scan_sum_float.restype = None
         L.oracle_scan_sum_float.argtypes = [ctypes.c_int, ctypes.c_int, i64, vp, vp, d, vp]
         _lib = L
@@ -143,6 +150,42 @@ def reduce(op, map_, x, y=None, out_dtype=None, return_sumabs=False):
     else:
         r = int(L.oracle_maxmin_int(op, map_, in_dt, n, _ptr(x), _ptr(y)))
     return (r, None) if return_sumabs else r
+
+
+MAP_CONJ_MUL = 3
+
+
+def axpbyz_complex(a, x, b, y):
+    """z = a*x + b*y for complex64/complex128 (PAPER.md:385-394 + R24): the
+    complex products written out component-wise, every operation RN, no FMA."""
+    x = np.ascontiguousarray(x)
+    y = np.ascontiguousarray(y, dtype=x.dtype)
+    assert x.dtype in (np.complex64, np.complex128) and x.shape == y.shape and x.ndim == 1
+    ct = x.dtype
+    av = np.array([a], dtype=ct)
+    bv = np.array([b], dtype=ct)
+    z = np.empty_like(x)
+    fn = lib().oracle_axpbyz_c64 if ct == np.complex64 else lib().oracle_axpbyz_c128
+    fn(x.size, av.ctypes.data, _ptr(x), bv.ctypes.data, _ptr(y), _ptr(z))
+    return z
+
+
+def reduce_complex(map_, x, y=None, return_sumabs=False):
+    """Complex sum (MAP_ID), dot (MAP_MUL: sum x*y), vdot (MAP_CONJ_MUL: sum
+    conj(x)*y) as a near-exact complex128; MAP_SQUARE gives sum |x_i|^2 as a
+    float64."""
+    x = np.ascontiguousarray(x)
+    is128 = int(x.dtype == np.complex128)
+    if map_ == MAP_SQUARE:
+        return lib().oracle_norm2_complex(is128, x.size, _ptr(x))
+    if map_ != MAP_ID:
+        y = np.ascontiguousarray(y, dtype=x.dtype)
+    out = np.zeros(2)
+    sa = ctypes.c_double(0.0)
+    lib().oracle_sum_complex(map_, is128, x.size, _ptr(x), _ptr(y) if map_ != MAP_ID else None, out.ctypes.data,
+                             ctypes.byref(sa))
+    r = complex(out[0], out[1])
+    return (r, sa.value) if return_sumabs else r
 
 
 NEUTRAL = {

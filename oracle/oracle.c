@@ -341,3 +341,97 @@ void oracle_scan_sum_float(int kind, int dt, int64_t n, const void *in, double *
     }
   }
 }
+
+/* ------------------------------------------------------------------------ */
+/* Complex numbers (§8(f) NEXT-3; "seamless support for complex numbers" in  */
+/* kernels and GPUArrays).  Arrays are interleaved         */
+/* (re, im) pairs of float (c64) or double (c128).                            */
+/*   axpbyz: z = a*x + b*y with the complex product written out as           */
+/*     re(u*v) = RN(RN(ur*vr) - RN(ui*vi)),  im(u*v) = RN(RN(ur*vi) + RN(ui*vr)) */
+/*     and component-wise RN additions (R24), no FMA contraction.             */
+/*   sum / dot (x*y) / vdot (conj(x)*y): exact-ish complex sums — each real   */
+/*     and imaginary term accumulated separately with Neumaier compensation   */
+/*     in float64 (c64 products are exact in float64; c128 products add     */
+/*     their fma error terms), returned as (re, im) doubles.                 */
+/*   norm2: sum |x_i|^2 = sum (xr^2 + xi^2), a real float64.                  */
+/* ------------------------------------------------------------------------ */
+enum { O_MAP_CONJ_MUL = 3 };
+
+void oracle_axpbyz_c64(int64_t n, const float *a, const float *x, const float *b, const float *y, float *z) {
+  for (int64_t i = 0; i < n; ++i) {
+    float xr = x[2 * i], xi = x[2 * i + 1], yr = y[2 * i], yi = y[2 * i + 1];
+    float p1 = a[0] * xr, p2 = a[1] * xi, p3 = a[0] * xi, p4 = a[1] * xr;
+    float axr = p1 - p2, axi = p3 + p4;
+    float q1 = b[0] * yr, q2 = b[1] * yi, q3 = b[0] * yi, q4 = b[1] * yr;
+    float byr = q1 - q2, byi = q3 + q4;
+    z[2 * i] = axr + byr;
+    z[2 * i + 1] = axi + byi;
+  }
+}
+
+void oracle_axpbyz_c128(int64_t n, const double *a, const double *x, const double *b, const double *y, double *z) {
+  for (int64_t i = 0; i < n; ++i) {
+    double xr = x[2 * i], xi = x[2 * i + 1], yr = y[2 * i], yi = y[2 * i + 1];
+    double p1 = a[0] * xr, p2 = a[1] * xi, p3 = a[0] * xi, p4 = a[1] * xr;
+    double axr = p1 - p2, axi = p3 + p4;
+    double q1 = b[0] * yr, q2 = b[1] * yi, q3 = b[0] * yi, q4 = b[1] * yr;
+    double byr = q1 - q2, byi = q3 + q4;
+    z[2 * i] = axr + byr;
+    z[2 * i + 1] = axi + byi;
+  }
+}
+
+/* add u*v (u, v doubles) exactly-ish: the product and, for doubles that are
+ * not exact products of floats, its fma error term */
+static void neumaier_add_prod(neumaier_t *acc, double u, double v, int exact) {
+  double p = u * v;
+  neumaier_add(acc, p);
+  if (!exact) neumaier_add(acc, fma(u, v, -p));
+}
+
+/* map: 0 = ID (sum), 1 = MUL (x*y), 3 = CONJ_MUL (conj(x)*y).  is_c128
+ * selects the element type.  out[0], out[1] = (re, im); sumabs[0] = sum of
+ * |terms| over both components. */
+void oracle_sum_complex(int map, int is_c128, int64_t n, const void *x, const void *y, double *out, double *sumabs) {
+  neumaier_t re = {0, 0}, im = {0, 0}, ab = {0, 0};
+  const int exact = !is_c128;
+  for (int64_t i = 0; i < n; ++i) {
+    double xr, xi, yr = 0, yi = 0;
+    if (is_c128) {
+      xr = ((const double *)x)[2 * i];
+      xi = ((const double *)x)[2 * i + 1];
+      if (map != O_MAP_ID) { yr = ((const double *)y)[2 * i]; yi = ((const double *)y)[2 * i + 1]; }
+    } else {
+      xr = ((const float *)x)[2 * i];
+      xi = ((const float *)x)[2 * i + 1];
+      if (map != O_MAP_ID) { yr = ((const float *)y)[2 * i]; yi = ((const float *)y)[2 * i + 1]; }
+    }
+    if (map == O_MAP_ID) {
+      neumaier_add(&re, xr);
+      neumaier_add(&im, xi);
+      neumaier_add(&ab, fabs(xr) + fabs(xi));
+    } else {
+      double s = (map == O_MAP_CONJ_MUL) ? -1.0 : 1.0; /* conj flips the sign of xi */
+      neumaier_add_prod(&re, xr, yr, exact);
+      neumaier_add_prod(&re, -s * xi, yi, exact);
+      neumaier_add_prod(&im, xr, yi, exact);
+      neumaier_add_prod(&im, s * xi, yr, exact);
+      neumaier_add(&ab, fabs(xr * yr) + fabs(xi * yi) + fabs(xr * yi) + fabs(xi * yr));
+    }
+  }
+  out[0] = re.s + re.c;
+  out[1] = im.s + im.c;
+  if (sumabs) *sumabs = ab.s + ab.c;
+}
+
+double oracle_norm2_complex(int is_c128, int64_t n, const void *x) {
+  neumaier_t acc = {0, 0};
+  const int exact = !is_c128;
+  for (int64_t i = 0; i < n; ++i) {
+    double xr = is_c128 ? ((const double *)x)[2 * i] : ((const float *)x)[2 * i];
+    double xi = is_c128 ? ((const double *)x)[2 * i + 1] : ((const float *)x)[2 * i + 1];
+    neumaier_add_prod(&acc, xr, xr, exact);
+    neumaier_add_prod(&acc, xi, xi, exact);
+  }
+  return acc.s + acc.c;
+}

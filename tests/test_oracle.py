@@ -416,3 +416,57 @@ def test_scan_float_sum_closed_forms():
     r = synth.host_fill(synth.F64_RAMP, 0, n)
     i = np.arange(n, dtype=np.float64)
     assert np.array_equal(oracle.scan(oracle.EXCLUSIVE, r), i * (i - 1) / 2)
+
+
+# ------------------------------------------------------------ complex (NEXT-3)
+def _cplx(dt, n, seed):
+    f = np.float32 if dt == np.complex64 else np.float64
+    r = synth.host_fill(synth.F32_S11 if f == np.float32 else synth.F64_S11, seed, 2 * n)
+    return r.view(dt)
+
+
+@pytest.mark.parametrize("dt", [np.complex64, np.complex128])
+def test_complex_axpbyz_matches_componentwise_numpy(dt):
+    """R24: re = RN(RN(ar xr) - RN(ai xi)) etc., re-derived here with numpy
+    real arithmetic (independent twin); a swapped sign or component fails."""
+    x = _cplx(dt, 5003, 1)
+    y = _cplx(dt, 5003, 2)
+    a, b = dt(1.5 - 2.25j), dt(-0.75 + 0.5j)
+    f = np.float32 if dt == np.complex64 else np.float64
+    ar, ai, br, bi = f(a.real), f(a.imag), f(b.real), f(b.imag)
+    xr, xi, yr, yi = x.real, x.imag, y.real, y.imag
+    zr = ((ar * xr) - (ai * xi)) + ((br * yr) - (bi * yi))
+    zi = ((ar * xi) + (ai * xr)) + ((br * yi) + (bi * yr))
+    z = oracle.axpbyz_complex(a, x, b, y)
+    assert bits_equal(z.real.copy(), zr) and bits_equal(z.imag.copy(), zi)
+    # closed forms: a=1, b=0 -> x; a=i, b=0 -> i*x = (-xi, xr)
+    assert bits_equal(oracle.axpbyz_complex(1, x, 0, y).view(f), (x + 0 * y).view(f))
+    iz = oracle.axpbyz_complex(1j, x, 0, y)
+    assert bits_equal(iz.real.copy(), -xi + f(0)) and bits_equal(iz.imag.copy(), xr + f(0))
+
+
+@pytest.mark.parametrize("dt", [np.complex64, np.complex128])
+def test_complex_sums_against_fraction_and_fsum(dt):
+    x = _cplx(dt, 20001, 3)
+    y = _cplx(dt, 20001, 4)
+    xc, yc = x.astype(np.complex128), y.astype(np.complex128)
+    # sum: fsum per component
+    s = oracle.reduce_complex(oracle.MAP_ID, x)
+    assert s.real == math.fsum(xc.real.tolist()) and s.imag == math.fsum(xc.imag.tolist())
+    # dot / vdot / norm2 on a small prefix with exact rational arithmetic
+    m = 50
+    fx = [(Fraction(float(v.real)), Fraction(float(v.imag))) for v in xc[:m]]
+    fy = [(Fraction(float(v.real)), Fraction(float(v.imag))) for v in yc[:m]]
+    dre = sum(a[0] * b[0] - a[1] * b[1] for a, b in zip(fx, fy))
+    dim = sum(a[0] * b[1] + a[1] * b[0] for a, b in zip(fx, fy))
+    vre = sum(a[0] * b[0] + a[1] * b[1] for a, b in zip(fx, fy))
+    vim = sum(a[0] * b[1] - a[1] * b[0] for a, b in zip(fx, fy))
+    n2 = sum(a[0] * a[0] + a[1] * a[1] for a in fx)
+    d = oracle.reduce_complex(oracle.MAP_MUL, x[:m], y[:m])
+    v = oracle.reduce_complex(oracle.MAP_CONJ_MUL, x[:m], y[:m])
+    assert d.real == float(dre) and d.imag == float(dim)
+    assert v.real == float(vre) and v.imag == float(vim)
+    assert oracle.reduce_complex(oracle.MAP_SQUARE, x[:m]) == float(n2)
+    # vdot(x, x) = |x|^2 (imaginary part exactly 0)
+    vv = oracle.reduce_complex(oracle.MAP_CONJ_MUL, x, x)
+    assert vv.imag == 0.0 and vv.real == pytest.approx(oracle.reduce_complex(oracle.MAP_SQUARE, x), rel=1e-15)
