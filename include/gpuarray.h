@@ -45,9 +45,11 @@
 extern "C" {
 #endif
 
-#define GPUARRAY_ABI_VERSION 1
+#define GPUARRAY_ABI_VERSION 2
 
-typedef enum { GA_F32 = 0, GA_F64 = 1, GA_I32 = 2, GA_I64 = 3 } ga_dtype_t;
+/* C64 / C128: complex numbers as interleaved (re, im) float / double pairs
+ * ("seamless support for complex numbers"; §8(f) NEXT-3). */
+typedef enum { GA_F32 = 0, GA_F64 = 1, GA_I32 = 2, GA_I64 = 3, GA_C64 = 4, GA_C128 = 5 } ga_dtype_t;
 
 /* Reduction expression "a+b", "max(a,b)", "min(a,b)" with its neutral element
  * (PAPER.md:479-485 and footnote): SUM 0; MAX -inf / INT_MIN; MIN +inf /
@@ -55,8 +57,9 @@ typedef enum { GA_F32 = 0, GA_F64 = 1, GA_I32 = 2, GA_I64 = 3 } ga_dtype_t;
 typedef enum { GA_OP_SUM = 0, GA_OP_MAX = 1, GA_OP_MIN = 2 } ga_op_t;
 
 /* Map expression over index i:
- * x[i] | x[i]*y[i] (dot) | x[i]*x[i] (squared 2-norm). */
-typedef enum { GA_MAP_ID = 0, GA_MAP_MUL = 1, GA_MAP_SQUARE = 2 } ga_map_t;
+ * x[i] | x[i]*y[i] (dot) | x[i]*x[i] (squared 2-norm; |x[i]|^2 for complex) |
+ * conj(x[i])*y[i] (vdot, complex only). */
+typedef enum { GA_MAP_ID = 0, GA_MAP_MUL = 1, GA_MAP_SQUARE = 2, GA_MAP_CONJ_MUL = 3 } ga_map_t;
 
 typedef enum { GA_SCAN_INCLUSIVE = 0, GA_SCAN_EXCLUSIVE = 1 } ga_scan_kind_t;
 
@@ -79,13 +82,16 @@ typedef struct ga_scalar {
     double f64;
     int32_t i32;
     int64_t i64;
+    float c64[2];   /* re, im */
+    double c128[2]; /* re, im */
   } v;
 } ga_scalar_t;
 
 /* z[i] = a*x[i] + b*y[i], i in [0, n).
  * Floats: z_i = RN(RN(a*x_i) + RN(b*y_i)) — two roundings of the products and
  * one of the sum, no FMA contraction (R1).  Integers wrap modulo
- * 2^w (R4).  dt in {F32, F64, I32, I64}.  z may equal x or y exactly
+ * 2^w (R4).  Complex: the products written out component-wise with every
+ * operation rounded (R24).  dt: any ga_dtype_t.  z may equal x or y exactly
  * (in-place); any other overlap is GA_ERR_INVALID_ARGUMENT.  n == 0: no-op. */
 ga_status_t gpuarray_axpbyz(ga_dtype_t dt, int64_t n, ga_scalar_t a, const void *x, ga_scalar_t b,
                             const void *y, void *z, void *stream);
@@ -107,8 +113,11 @@ size_t gpuarray_reduce_workspace_bytes(ga_dtype_t out_dt, int64_t n);
  * Supported (in_dt -> out_dt):
  *   SUM: F32->F32, F32->F64, F64->F64, I32->I32, I32->I64, I64->I64
  *        (accumulation in out_dt; integer maps widen to out_dt then wrap, R3/R4)
- *   MAX, MIN: out_dt == in_dt; the map is evaluated in in_dt (RN(x*y), wrap).
- * y must be non-NULL iff map == GA_MAP_MUL (it is ignored otherwise).
+ *   SUM over complex: C64->C64, C128->C128 with MAP_ID / MAP_MUL (dot) /
+ *        MAP_CONJ_MUL (vdot); MAP_SQUARE gives sum |x|^2: C64->F32, C128->F64
+ *   MAX, MIN: real dtypes, out_dt == in_dt; the map is evaluated in in_dt
+ *        (RN(x*y), wrap).
+ * y must be non-NULL iff map is MAP_MUL or MAP_CONJ_MUL (ignored otherwise).
  * Float SUM is a tree-ordered sum (not the exact sum): deterministic for a
  * given (n, device), accurate as DESIGN.md R9/R10 state.  n == 0 writes the
  * neutral element. */
@@ -118,9 +127,9 @@ ga_status_t gpuarray_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype
 
 /* ---- Fused cross-GPU finish (§8(a) a6 in one kernel).
  * Bytes of the per-rank exchange buffer gpuarray_reduce_xgpu needs (2 x 64
- * slots of 16 bytes).  Every rank allocates one in memory all ranks can
+ * slots of 32 bytes).  Every rank allocates one in memory all ranks can
  * address (torch symmetric memory over NVLink / NVSwitch), zero-filled once. */
-size_t gpuarray_xgpu_buffer_bytes(void);
+size_t gpuarray_xgpu_buffer_bytes(void);   /* 2 x 64 slots of 32 bytes */
 
 /* What the cross-GPU finish folds: every rank's result (a global reduction),
  * or only the ranks before this one, in rank order (the exclusive prefix over
@@ -155,7 +164,7 @@ ga_status_t gpuarray_reduce_xgpu(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_
 size_t gpuarray_scan_workspace_bytes(ga_dtype_t dt, int64_t n);
 
 /* Scan with the reduction expression op ∈ {SUM, MAX, MIN} (written ⊕ below),
- * dt in {F32, F64, I32, I64}:
+ * dt in {F32, F64, I32, I64} (complex: GA_ERR_UNSUPPORTED):
  *   inclusive: out[i] = c ⊕ in[0] ⊕ ... ⊕ in[i]
  *   exclusive: out[0] = c, out[i] = c ⊕ in[0] ⊕ ... ⊕ in[i-1]   (R13)
  * where c = carry[0] ⊕ ... ⊕ carry[carry_count-1] (a device array of dt; c is

@@ -7,6 +7,7 @@ Importing requires the built CUDA library (libgpuarray.so); there is no CPU
 fallback.  See DESIGN.md."""
 from . import gpuarray  # noqa: F401
 from .gpuarray import (axpbyz, axpbz, dot, launch_count, max, min, norm2sq, reduce, scan,  # noqa: F401
-                       sum)
+                       sum, vdot)
 
-__all__ = ["gpuarray", "axpbyz", "axpbz", "reduce", "dot", "sum", "norm2sq", "max", "min", "scan", "launch_count"]
+__all__ = ["gpuarray", "axpbyz", "axpbz", "reduce", "dot", "vdot", "sum", "norm2sq", "max", "min", "scan",
+           "launch_count"]

@@ -11,9 +11,9 @@ import os
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libgpuarray.so")
 
-GA_F32, GA_F64, GA_I32, GA_I64 = 0, 1, 2, 3
+GA_F32, GA_F64, GA_I32, GA_I64, GA_C64, GA_C128 = 0, 1, 2, 3, 4, 5
 GA_OP_SUM, GA_OP_MAX, GA_OP_MIN = 0, 1, 2
-GA_MAP_ID, GA_MAP_MUL, GA_MAP_SQUARE = 0, 1, 2
+GA_MAP_ID, GA_MAP_MUL, GA_MAP_SQUARE, GA_MAP_CONJ_MUL = 0, 1, 2, 3
 GA_SCAN_INCLUSIVE, GA_SCAN_EXCLUSIVE = 0, 1
 GA_OK, GA_ERR_INVALID_ARGUMENT, GA_ERR_UNSUPPORTED, GA_ERR_WORKSPACE, GA_ERR_CUDA = 0, 1, 2, 3, 4
 
@@ -26,10 +26,12 @@ EXPORTS = (
 
 
 class ga_scalar_t(ctypes.Structure):
-    """Layout-identical to the C struct: {int32 dtype; int32 reserved; union v}.
-    The union is carried as its 8 raw bytes (little-endian: a 4-byte member sits
-    in the low half) because ctypes cannot pass unions by value portably."""
-    _fields_ = [("dtype", ctypes.c_int32), ("reserved", ctypes.c_int32), ("bits", ctypes.c_uint64)]
+    """Layout-identical to the C struct: {int32 dtype; int32 reserved; union v}
+    (24 bytes).  The 16-byte union is carried as two raw 8-byte words
+    (little-endian: a 4-byte member sits in the low half of `bits`) because
+    ctypes cannot pass unions by value portably."""
+    _fields_ = [("dtype", ctypes.c_int32), ("reserved", ctypes.c_int32), ("bits", ctypes.c_uint64),
+                ("bits_hi", ctypes.c_uint64)]
 
 
 def make_scalar(dt, value):
@@ -43,12 +45,19 @@ def make_scalar(dt, value):
         raw = struct.pack("<i", ((int(value) + (1 << 31)) % (1 << 32)) - (1 << 31)) + b"\0\0\0\0"
     elif dt == GA_I64:
         raw = struct.pack("<q", ((int(value) + (1 << 63)) % (1 << 64)) - (1 << 63))
+    elif dt == GA_C64:
+        c = complex(value)
+        raw = struct.pack("<ff", c.real, c.imag)
+    elif dt == GA_C128:
+        c = complex(value)
+        raw = struct.pack("<dd", c.real, c.imag)
     else:
         raise ValueError(f"bad dtype {dt}")
+    raw = raw.ljust(16, b"\0")
     s = ga_scalar_t()
     s.dtype = dt
     s.reserved = 0
-    s.bits = struct.unpack("<Q", raw)[0]
+    s.bits, s.bits_hi = struct.unpack("<QQ", raw)
     return s
 
 

@@ -54,12 +54,12 @@ __global__ void __launch_bounds__(EW_BLOCK) ew_vec_kernel(EwArgs<T> p) {
   // Scalar head (to 32 B alignment) and tail (remainder of the body).
   const int64_t tail0 = p.head + p.nvec * VEC;
   if (tid < p.head) {
-    T y = HAS_Y ? p.y[tid] : T(0);
+    T y = HAS_Y ? p.y[tid] : zero_of<T>();
     p.z[tid] = stmt<T, HAS_Y>(p.a, p.x[tid], p.b, y);
   }
   if (tid < p.n - tail0) {
     int64_t i = tail0 + tid;
-    T y = HAS_Y ? p.y[i] : T(0);
+    T y = HAS_Y ? p.y[i] : zero_of<T>();
     p.z[i] = stmt<T, HAS_Y>(p.a, p.x[i], p.b, y);
   }
 
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(EW_BLOCK) ew_vec_kernel(EwArgs<T> p) {
         V32 vz;
 #pragma unroll
         for (int k = 0; k < VEC; ++k) {
-          T y = HAS_Y ? vget<T>(vy[j], k) : T(0);
+          T y = HAS_Y ? vget<T>(vy[j], k) : zero_of<T>();
           vset<T>(vz, k, stmt<T, HAS_Y>(p.a, vget<T>(vx[j], k), p.b, y));
         }
         st_256(zb + v * 32, vz);
@@ -101,7 +101,7 @@ template <typename T, bool HAS_Y>
 __global__ void __launch_bounds__(EW_BLOCK) ew_scalar_kernel(EwArgs<T> p) {
   const int64_t nthreads = (int64_t)gridDim.x * EW_BLOCK;
   for (int64_t i = (int64_t)blockIdx.x * EW_BLOCK + threadIdx.x; i < p.n; i += nthreads) {
-    T y = HAS_Y ? p.y[i] : T(0);
+    T y = HAS_Y ? p.y[i] : zero_of<T>();
     p.z[i] = stmt<T, HAS_Y>(p.a, p.x[i], p.b, y);
   }
 }
@@ -116,6 +116,10 @@ template <>
 int32_t scalar_value<int32_t>(const ga_scalar_t &s) { return s.v.i32; }
 template <>
 int64_t scalar_value<int64_t>(const ga_scalar_t &s) { return s.v.i64; }
+template <>
+c64 scalar_value<c64>(const ga_scalar_t &s) { return c64{s.v.c64[0], s.v.c64[1]}; }
+template <>
+c128 scalar_value<c128>(const ga_scalar_t &s) { return c128{s.v.c128[0], s.v.c128[1]}; }
 
 template <typename T, bool HAS_Y>
 ga_status_t launch_ew(int64_t n, const ga_scalar_t &a, const void *x, const ga_scalar_t &b, const void *y,
@@ -164,6 +168,8 @@ ga_status_t launch_axpbyz(ga_dtype_t dt, int64_t n, const ga_scalar_t &a, const 
     case GA_F64: return launch_ew<double, true>(n, a, x, b, y, z, s);
     case GA_I32: return launch_ew<int32_t, true>(n, a, x, b, y, z, s);
     case GA_I64: return launch_ew<int64_t, true>(n, a, x, b, y, z, s);
+    case GA_C64: return launch_ew<c64, true>(n, a, x, b, y, z, s);
+    case GA_C128: return launch_ew<c128, true>(n, a, x, b, y, z, s);
   }
   return fail(GA_ERR_INVALID_ARGUMENT, "bad dtype %d", (int)dt);
 }
@@ -175,6 +181,8 @@ ga_status_t launch_axpbz(ga_dtype_t dt, int64_t n, const ga_scalar_t &a, const v
     case GA_F64: return launch_ew<double, false>(n, a, x, b, nullptr, z, s);
     case GA_I32: return launch_ew<int32_t, false>(n, a, x, b, nullptr, z, s);
     case GA_I64: return launch_ew<int64_t, false>(n, a, x, b, nullptr, z, s);
+    case GA_C64: return launch_ew<c64, false>(n, a, x, b, nullptr, z, s);
+    case GA_C128: return launch_ew<c128, false>(n, a, x, b, nullptr, z, s);
   }
   return fail(GA_ERR_INVALID_ARGUMENT, "bad dtype %d", (int)dt);
 }

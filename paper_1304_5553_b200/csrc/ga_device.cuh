@@ -48,6 +48,20 @@ __device__ __forceinline__ void st_256(void *p, const V32 &v) {
                : "memory");
 }
 
+// Complex element types (interleaved re, im), §8(f) NEXT-3.
+struct alignas(8) c64 {
+  float re, im;
+};
+struct alignas(16) c128 {
+  double re, im;
+};
+template <typename T>
+struct is_complex : std::false_type {};
+template <>
+struct is_complex<c64> : std::true_type {};
+template <>
+struct is_complex<c128> : std::true_type {};
+
 template <bool NC>
 __device__ __forceinline__ V32 ld_vec(const void *p) {
   if constexpr (NC) return ld_nc_256(p);
@@ -70,6 +84,16 @@ __device__ __forceinline__ int64_t vget<int64_t>(const V32 &v, int k) {
   return (int64_t)(((uint64_t)v.r[2 * k + 1] << 32) | v.r[2 * k]);
 }
 
+template <>
+__device__ __forceinline__ c64 vget<c64>(const V32 &v, int k) {
+  return c64{__uint_as_float(v.r[2 * k]), __uint_as_float(v.r[2 * k + 1])};
+}
+template <>
+__device__ __forceinline__ c128 vget<c128>(const V32 &v, int k) {
+  return c128{__hiloint2double((int)v.r[4 * k + 1], (int)v.r[4 * k]),
+              __hiloint2double((int)v.r[4 * k + 3], (int)v.r[4 * k + 2])};
+}
+
 template <typename T>
 __device__ __forceinline__ void vset(V32 &v, int k, T x);
 template <>
@@ -87,6 +111,19 @@ __device__ __forceinline__ void vset<int64_t>(V32 &v, int k, int64_t x) {
   v.r[2 * k + 1] = (uint32_t)((uint64_t)x >> 32);
 }
 
+template <>
+__device__ __forceinline__ void vset<c64>(V32 &v, int k, c64 x) {
+  v.r[2 * k] = __float_as_uint(x.re);
+  v.r[2 * k + 1] = __float_as_uint(x.im);
+}
+template <>
+__device__ __forceinline__ void vset<c128>(V32 &v, int k, c128 x) {
+  v.r[4 * k] = (uint32_t)__double2loint(x.re);
+  v.r[4 * k + 1] = (uint32_t)__double2hiint(x.re);
+  v.r[4 * k + 2] = (uint32_t)__double2loint(x.im);
+  v.r[4 * k + 3] = (uint32_t)__double2hiint(x.im);
+}
+
 // ---------------------------------------------------------------------------
 // Element arithmetic with the rounding sequence DESIGN.md R1 fixes:
 // mul = RN(a*b), add = RN(a+b), never contracted to FMA.  Integers wrap.
@@ -101,6 +138,18 @@ __device__ __forceinline__ int32_t e_add(int32_t a, int32_t b) { return (int32_t
 __device__ __forceinline__ int64_t e_add(int64_t a, int64_t b) { return (int64_t)((uint64_t)a + (uint64_t)b); }
 __device__ __forceinline__ int32_t e_sub(int32_t a, int32_t b) { return (int32_t)((uint32_t)a - (uint32_t)b); }
 __device__ __forceinline__ int64_t e_sub(int64_t a, int64_t b) { return (int64_t)((uint64_t)a - (uint64_t)b); }
+// Complex (R24): the product written out component-wise, every operation RN:
+// re(u*v) = RN(RN(ur*vr) - RN(ui*vi)), im(u*v) = RN(RN(ur*vi) + RN(ui*vr)).
+__device__ __forceinline__ c64 e_mul(c64 u, c64 v) {
+  return c64{__fsub_rn(__fmul_rn(u.re, v.re), __fmul_rn(u.im, v.im)),
+             __fadd_rn(__fmul_rn(u.re, v.im), __fmul_rn(u.im, v.re))};
+}
+__device__ __forceinline__ c128 e_mul(c128 u, c128 v) {
+  return c128{__dsub_rn(__dmul_rn(u.re, v.re), __dmul_rn(u.im, v.im)),
+              __dadd_rn(__dmul_rn(u.re, v.im), __dmul_rn(u.im, v.re))};
+}
+__device__ __forceinline__ c64 e_add(c64 u, c64 v) { return c64{__fadd_rn(u.re, v.re), __fadd_rn(u.im, v.im)}; }
+__device__ __forceinline__ c128 e_add(c128 u, c128 v) { return c128{__dadd_rn(u.re, v.re), __dadd_rn(u.im, v.im)}; }
 // Fused multiply-add (one rounding) — used only where a tolerance, not
 // bit-exactness, is the contract (float SUM reductions, R9).
 __device__ __forceinline__ float e_fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
@@ -137,8 +186,14 @@ template <int OP, typename T>
 struct Op;
 
 template <typename T>
+__device__ __forceinline__ T zero_of() {
+  if constexpr (is_complex<T>::value) return T{0, 0};
+  else return T(0);
+}
+
+template <typename T>
 struct Op<GA_OP_SUM, T> {
-  __device__ static T neutral() { return T(0); }
+  __device__ static T neutral() { return zero_of<T>(); }
   __device__ static T fold(T a, T b) { return e_add(a, b); }
 };
 template <typename T>
@@ -160,12 +215,26 @@ struct Op<GA_OP_MIN, T> {
   }
 };
 
+// Warp shuffle for scalar and complex elements.
+template <typename T>
+__device__ __forceinline__ T shfl_xor(T v, int off) {
+  if constexpr (is_complex<T>::value)
+    return T{__shfl_xor_sync(0xffffffffu, v.re, off), __shfl_xor_sync(0xffffffffu, v.im, off)};
+  else return __shfl_xor_sync(0xffffffffu, v, off);
+}
+// L2 load (bypassing L1) of scalar and complex elements.
+template <typename T>
+__device__ __forceinline__ T ldcg(const T *p) {
+  if constexpr (is_complex<T>::value) return T{__ldcg(&p->re), __ldcg(&p->im)};
+  else return __ldcg(p);
+}
+
 // Warp-wide fold with a fixed xor-butterfly order: every lane ends with the
 // same value, bit-identical run to run.
 template <int OP, typename T>
 __device__ __forceinline__ T warp_fold(T v) {
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v = Op<OP, T>::fold(v, __shfl_xor_sync(0xffffffffu, v, off));
+  for (int off = 16; off > 0; off >>= 1) v = Op<OP, T>::fold(v, shfl_xor<T>(v, off));
   return v;
 }
 

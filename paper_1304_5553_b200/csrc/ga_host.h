@@ -23,9 +23,11 @@ int resident_grid(const void *kernel, int block, size_t dyn_smem = 0);
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-inline size_t dtype_size(ga_dtype_t dt) { return (dt == GA_F32 || dt == GA_I32) ? 4 : 8; }
+inline size_t dtype_size(ga_dtype_t dt) {
+  return (dt == GA_F32 || dt == GA_I32) ? 4 : dt == GA_C128 ? 16 : 8;
+}
 
-inline bool valid_dtype(int dt) { return dt >= GA_F32 && dt <= GA_I64; }
+inline bool valid_dtype(int dt) { return dt >= GA_F32 && dt <= GA_C128; }
 
 // [p, p+bytes) and [q, q+bytes2) overlap without being the same start.
 inline bool partial_overlap(const void *p, size_t bytes, const void *q, size_t bytes2) {
@@ -38,6 +40,7 @@ inline bool partial_overlap(const void *p, size_t bytes, const void *q, size_t b
 // `world` exchange-buffer pointers (one per rank, NVLink-mapped), own rank,
 // and the call's sequence number (identical on all ranks, >= 1).
 constexpr int XG_MAX_WORLD = 64;
+constexpr int XG_SLOT = 32;  // bytes per exchange slot: value (<= 16 B) + seq at +16
 struct Exchange {
   const unsigned long long *peers = nullptr;
   int rank = 0;

@@ -106,31 +106,33 @@ size_t gpuarray_reduce_workspace_bytes(ga_dtype_t out_dt, int64_t n) {
 ga_status_t gpuarray_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n, const void *x,
                             const void *y, void *out, void *workspace, size_t workspace_bytes, void *stream) {
   if (op < GA_OP_SUM || op > GA_OP_MIN) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: bad op %d", (int)op);
-  if (map < GA_MAP_ID || map > GA_MAP_SQUARE) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: bad map %d", (int)map);
+  if (map < GA_MAP_ID || map > GA_MAP_CONJ_MUL) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: bad map %d", (int)map);
   if (!valid_dtype(in_dt) || !valid_dtype(out_dt)) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: bad dtype");
   if (n < 0) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: n < 0");
   if (!out) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: out is NULL");
   if (n > 0 && !x) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: x is NULL with n > 0");
-  if (map == GA_MAP_MUL && n > 0 && !y) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: MAP_MUL needs y");
+  const bool has_y = map == GA_MAP_MUL || map == GA_MAP_CONJ_MUL;
+  if (has_y && n > 0 && !y) return fail(GA_ERR_INVALID_ARGUMENT, "reduce: MAP_MUL / MAP_CONJ_MUL need y");
   if (!workspace || workspace_bytes < reduce_workspace_bytes())
     return fail(GA_ERR_WORKSPACE, "reduce: workspace needs %zu bytes", reduce_workspace_bytes());
-  return launch_reduce(op, map, in_dt, out_dt, n, x, map == GA_MAP_MUL ? y : nullptr, out, workspace, Exchange(),
+  return launch_reduce(op, map, in_dt, out_dt, n, x, has_y ? y : nullptr, out, workspace, Exchange(),
                        (cudaStream_t)stream);
 }
 
-size_t gpuarray_xgpu_buffer_bytes(void) { return (size_t)2 * XG_MAX_WORLD * 16; }
+size_t gpuarray_xgpu_buffer_bytes(void) { return (size_t)2 * XG_MAX_WORLD * XG_SLOT; }
 
 ga_status_t gpuarray_reduce_xgpu(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
                                  const void *x, const void *y, void *out, void *workspace, size_t workspace_bytes,
                                  const uint64_t *peer_buffers, int rank, int world, uint64_t seq,
                                  ga_xgpu_fold_t fold, void *stream) {
   if (op < GA_OP_SUM || op > GA_OP_MIN) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: bad op %d", (int)op);
-  if (map < GA_MAP_ID || map > GA_MAP_SQUARE) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: bad map");
+  if (map < GA_MAP_ID || map > GA_MAP_CONJ_MUL) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: bad map");
   if (!valid_dtype(in_dt) || !valid_dtype(out_dt)) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: bad dtype");
   if (n < 0) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: n < 0");
   if (!out) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: out is NULL");
   if (n > 0 && !x) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: x is NULL with n > 0");
-  if (map == GA_MAP_MUL && n > 0 && !y) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: MAP_MUL needs y");
+  const bool has_y = map == GA_MAP_MUL || map == GA_MAP_CONJ_MUL;
+  if (has_y && n > 0 && !y) return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: MAP_MUL / MAP_CONJ_MUL need y");
   if (world < 1 || world > XG_MAX_WORLD || rank < 0 || rank >= world || !peer_buffers || seq == 0)
     return fail(GA_ERR_INVALID_ARGUMENT, "reduce_xgpu: bad rank/world/peers/seq");
   if (fold != GA_XGPU_ALL && fold != GA_XGPU_EXCLUSIVE_PREFIX)
@@ -143,7 +145,7 @@ ga_status_t gpuarray_reduce_xgpu(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_
   xg.world = world;
   xg.seq = seq;
   xg.prefix_only = fold == GA_XGPU_EXCLUSIVE_PREFIX;
-  return launch_reduce(op, map, in_dt, out_dt, n, x, map == GA_MAP_MUL ? y : nullptr, out, workspace, xg,
+  return launch_reduce(op, map, in_dt, out_dt, n, x, has_y ? y : nullptr, out, workspace, xg,
                        (cudaStream_t)stream);
 }
 
@@ -156,6 +158,7 @@ ga_status_t gpuarray_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_
   if (kind != GA_SCAN_INCLUSIVE && kind != GA_SCAN_EXCLUSIVE)
     return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad kind %d", (int)kind);
   if (!valid_dtype(dt)) return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad dtype %d", (int)dt);
+  if (dt == GA_C64 || dt == GA_C128) return fail(GA_ERR_UNSUPPORTED, "scan: complex not instantiated");
   if (n < 0) return fail(GA_ERR_INVALID_ARGUMENT, "scan: n < 0");
   if (carry_count < 0 || (carry_count > 0 && !carry))
     return fail(GA_ERR_INVALID_ARGUMENT, "scan: carry_count < 0 or carry NULL");

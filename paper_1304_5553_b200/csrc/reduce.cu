@@ -50,7 +50,7 @@ ga_status_t run(int64_t n, const void *x, const void *y, void *out, void *ws, co
     return check_launch("neutral_kernel");
   }
   constexpr int VEC = 32 / sizeof(Tin);
-  constexpr int UNROLL = (MAP == GA_MAP_MUL) ? 4 : 8;
+  constexpr int UNROLL = (MAP == GA_MAP_MUL || MAP == GA_MAP_CONJ_MUL) ? 4 : 8;
   RedArgs<Tin, Tacc> p;
   p.n = n;
   p.x = static_cast<const Tin *>(x);
@@ -61,7 +61,8 @@ ga_status_t run(int64_t n, const void *x, const void *y, void *out, void *ws, co
   p.xg = xg;
 
   const uintptr_t phase = (uintptr_t)x & 31;
-  const bool coaligned = (MAP != GA_MAP_MUL || ((uintptr_t)y & 31) == phase) && (phase % sizeof(Tin)) == 0;
+  constexpr bool HAS_Y = MAP == GA_MAP_MUL || MAP == GA_MAP_CONJ_MUL;
+  const bool coaligned = (!HAS_Y || ((uintptr_t)y & 31) == phase) && (phase % sizeof(Tin)) == 0;
   if (coaligned) {
     p.head = std::min<int64_t>(n, (int64_t)(((32 - phase) & 31) / sizeof(Tin)));
     p.nvec = (n - p.head) / VEC;
@@ -84,8 +85,28 @@ ga_status_t by_map(ga_map_t map, int64_t n, const void *x, const void *y, void *
                    cudaStream_t s) {
   switch (map) {
     case GA_MAP_ID: return run<Tin, Tacc, OP, GA_MAP_ID>(n, x, y, out, ws, xg, s);
-    case GA_MAP_MUL: return run<Tin, Tacc, OP, GA_MAP_MUL>(n, x, y, out, ws, xg, s);
+    case GA_MAP_MUL:
+    case GA_MAP_CONJ_MUL:  // conj(x) == x for real x
+      return run<Tin, Tacc, OP, GA_MAP_MUL>(n, x, y, out, ws, xg, s);
     case GA_MAP_SQUARE: return run<Tin, Tacc, OP, GA_MAP_SQUARE>(n, x, y, out, ws, xg, s);
+  }
+  return fail(GA_ERR_INVALID_ARGUMENT, "bad map %d", (int)map);
+}
+
+// Complex SUM: x | x*y | conj(x)*y into the complex type; |x|^2 into the real one.
+template <typename C, typename R>
+ga_status_t complex_sum(ga_map_t map, ga_dtype_t out_dt, ga_dtype_t cdt, ga_dtype_t rdt, int64_t n, const void *x,
+                        const void *y, void *out, void *ws, const Exchange &xg, cudaStream_t s) {
+  if (map == GA_MAP_SQUARE) {
+    if (out_dt != rdt) return fail(GA_ERR_UNSUPPORTED, "complex |x|^2 sums into the real type");
+    return run<C, R, GA_OP_SUM, GA_MAP_SQUARE>(n, x, y, out, ws, xg, s);
+  }
+  if (out_dt != cdt) return fail(GA_ERR_UNSUPPORTED, "complex SUM needs out_dt == in_dt");
+  switch (map) {
+    case GA_MAP_ID: return run<C, C, GA_OP_SUM, GA_MAP_ID>(n, x, y, out, ws, xg, s);
+    case GA_MAP_MUL: return run<C, C, GA_OP_SUM, GA_MAP_MUL>(n, x, y, out, ws, xg, s);
+    case GA_MAP_CONJ_MUL: return run<C, C, GA_OP_SUM, GA_MAP_CONJ_MUL>(n, x, y, out, ws, xg, s);
+    default: break;
   }
   return fail(GA_ERR_INVALID_ARGUMENT, "bad map %d", (int)map);
 }
@@ -98,10 +119,15 @@ ga_status_t maxmin(ga_map_t map, int64_t n, const void *x, const void *y, void *
 
 }  // namespace
 
-size_t reduce_workspace_bytes() { return RED_HEADER + (size_t)RED_MAX_PARTIALS * 8; }
+size_t reduce_workspace_bytes() { return RED_HEADER + (size_t)RED_MAX_PARTIALS * 16; }  // up to c128 partials
 
 ga_status_t launch_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
                           const void *x, const void *y, void *out, void *ws, const Exchange &xg, cudaStream_t s) {
+  if (in_dt == GA_C64 || in_dt == GA_C128) {
+    if (op != GA_OP_SUM) return fail(GA_ERR_UNSUPPORTED, "MAX/MIN are not defined for complex numbers");
+    if (in_dt == GA_C64) return complex_sum<c64, float>(map, out_dt, GA_C64, GA_F32, n, x, y, out, ws, xg, s);
+    return complex_sum<c128, double>(map, out_dt, GA_C128, GA_F64, n, x, y, out, ws, xg, s);
+  }
   if (op == GA_OP_SUM) {
     if (in_dt == GA_F32 && out_dt == GA_F32) return by_map<float, float, GA_OP_SUM>(map, n, x, y, out, ws, xg, s);
     if (in_dt == GA_F32 && out_dt == GA_F64) return by_map<float, double, GA_OP_SUM>(map, n, x, y, out, ws, xg, s);
@@ -118,6 +144,7 @@ ga_status_t launch_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t
       case GA_F64: return maxmin<double, GA_OP_MAX>(map, n, x, y, out, ws, xg, s);
       case GA_I32: return maxmin<int32_t, GA_OP_MAX>(map, n, x, y, out, ws, xg, s);
       case GA_I64: return maxmin<int64_t, GA_OP_MAX>(map, n, x, y, out, ws, xg, s);
+      default: break;
     }
   } else if (op == GA_OP_MIN) {
     switch (in_dt) {
@@ -125,6 +152,7 @@ ga_status_t launch_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t
       case GA_F64: return maxmin<double, GA_OP_MIN>(map, n, x, y, out, ws, xg, s);
       case GA_I32: return maxmin<int32_t, GA_OP_MIN>(map, n, x, y, out, ws, xg, s);
       case GA_I64: return maxmin<int64_t, GA_OP_MIN>(map, n, x, y, out, ws, xg, s);
+      default: break;
     }
   }
   return fail(GA_ERR_INVALID_ARGUMENT, "bad op %d", (int)op);

@@ -27,9 +27,29 @@ __host__ __device__ constexpr bool is_fp() {
 // (exact product, one rounding): the tolerance of DESIGN.md R9/R10 applies.
 // SUM over integers widens to Tacc, then wraps (R3, R4).  MAX/MIN evaluate
 // the map in Tin with RN / wrap (R3) and fold with maxNum/minNum (R6).
+// Complex SUM (NEXT-3): x | x*y | conj(x)*y accumulated with FMAs per
+// component (tolerance-governed, like real float SUM); x*x under SQUARE means
+// |x|^2 into a real accumulator.
+template <typename Tin, typename Tacc, int MAP>
+__device__ __forceinline__ Tacc map_acc_complex(Tacc acc, Tin x, Tin y) {
+  if constexpr (!is_complex<Tacc>::value) {  // |x|^2
+    return e_fma(x.im, x.im, e_fma(x.re, x.re, acc));
+  } else if constexpr (MAP == GA_MAP_ID) {
+    return e_add(acc, x);
+  } else {
+    const decltype(x.re) s = MAP == GA_MAP_CONJ_MUL ? -1 : 1;  // conj flips the sign of x.im
+    Tacc r;
+    r.re = e_fma(-s * x.im, y.im, e_fma(x.re, y.re, acc.re));
+    r.im = e_fma(s * x.im, y.re, e_fma(x.re, y.im, acc.im));
+    return r;
+  }
+}
+
 template <typename Tin, typename Tacc, int OP, int MAP>
 __device__ __forceinline__ Tacc map_acc(Tacc acc, Tin x, Tin y) {
-  if constexpr (OP == GA_OP_SUM) {
+  if constexpr (is_complex<Tin>::value) {
+    return map_acc_complex<Tin, Tacc, MAP>(acc, x, y);
+  } else if constexpr (OP == GA_OP_SUM) {
     const Tacc u = (Tacc)x;
     if constexpr (is_fp<Tacc>()) {
       if constexpr (MAP == GA_MAP_ID) return e_add(acc, u);
@@ -76,22 +96,22 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
 // pointers: NVLink-mapped symmetric memory), then wait for all `world` slots
 // of the own buffer and fold them in rank order, so every rank computes the
 // same bits with no separate collective launch (prefix_only: the fold of the
-// ranks before this one — the offset of a sharded scan).  Slot entry = {value: 8 B,
-// seq: 8 B}; slots are double-buffered by seq parity (a rank cannot publish
-// call seq+2 before every rank has read call seq).
+// ranks before this one — the offset of a sharded scan).  Slot entry (32 B) =
+// {value: 16 B, seq: 8 B, pad}; slots are double-buffered by seq parity (a
+// rank cannot publish call seq+2 before every rank has read call seq).
 template <int OP, typename Tacc>
 __device__ Tacc exchange_fold(const Exchange &xg, Tacc local) {
   const int par = (int)(xg.seq & 1);
   for (int r = 0; r < xg.world; ++r) {
-    char *e = reinterpret_cast<char *>(xg.peers[r]) + ((size_t)par * XG_MAX_WORLD + xg.rank) * 16;
+    char *e = reinterpret_cast<char *>(xg.peers[r]) + ((size_t)par * XG_MAX_WORLD + xg.rank) * XG_SLOT;
     *reinterpret_cast<Tacc *>(e) = local;
-    st_release_sys_u64(reinterpret_cast<unsigned long long *>(e + 8), xg.seq);
+    st_release_sys_u64(reinterpret_cast<unsigned long long *>(e + 16), xg.seq);
   }
   const char *own = reinterpret_cast<const char *>(xg.peers[xg.rank]);
   Tacc v = Op<OP, Tacc>::neutral();
   for (int r = 0; r < xg.world; ++r) {
-    const char *e = own + ((size_t)par * XG_MAX_WORLD + r) * 16;
-    const unsigned long long *f = reinterpret_cast<const unsigned long long *>(e + 8);
+    const char *e = own + ((size_t)par * XG_MAX_WORLD + r) * XG_SLOT;
+    const unsigned long long *f = reinterpret_cast<const unsigned long long *>(e + 16);
     uint32_t spins = 0;
     uint64_t t0 = 0;
     while (ld_acquire_sys_u64(f) != xg.seq) {
@@ -103,7 +123,7 @@ __device__ Tacc exchange_fold(const Exchange &xg, Tacc local) {
       }
     }
     // every rank is waited for (slot-reuse safety); prefix_only folds r < rank
-    if (!xg.prefix_only || r < xg.rank) v = Op<OP, Tacc>::fold(v, *reinterpret_cast<const volatile Tacc *>(e));
+    if (!xg.prefix_only || r < xg.rank) v = Op<OP, Tacc>::fold(v, ldcg<Tacc>(reinterpret_cast<const Tacc *>(e)));
   }
   return v;
 }
@@ -125,7 +145,7 @@ __device__ __forceinline__ T block_fold(T v, T *smem) {
 template <typename Tin, typename Tacc, int OP, int MAP, int UNROLL, int RED_BLOCK, int MINB>
 __global__ void __launch_bounds__(RED_BLOCK, MINB) reduce_kernel(RedArgs<Tin, Tacc> p) {
   constexpr int VEC = 32 / sizeof(Tin);
-  constexpr bool HAS_Y = MAP == GA_MAP_MUL;
+  constexpr bool HAS_Y = MAP == GA_MAP_MUL || MAP == GA_MAP_CONJ_MUL;
   __shared__ Tacc smem[RED_BLOCK / 32];
   __shared__ bool is_last;
 
@@ -139,10 +159,10 @@ __global__ void __launch_bounds__(RED_BLOCK, MINB) reduce_kernel(RedArgs<Tin, Ta
   // Scalar parts: the unaligned head (all of x when x/y are not co-aligned)
   // and the tail after the last whole vector.
   for (int64_t i = tid; i < p.head; i += nthreads)
-    acc[0] = map_acc<Tin, Tacc, OP, MAP>(acc[0], p.x[i], HAS_Y ? p.y[i] : Tin(0));
+    acc[0] = map_acc<Tin, Tacc, OP, MAP>(acc[0], p.x[i], HAS_Y ? p.y[i] : zero_of<Tin>());
   const int64_t tail0 = p.head + p.nvec * VEC;
   for (int64_t i = tail0 + tid; i < p.n; i += nthreads)
-    acc[VEC - 1] = map_acc<Tin, Tacc, OP, MAP>(acc[VEC - 1], p.x[i], HAS_Y ? p.y[i] : Tin(0));
+    acc[VEC - 1] = map_acc<Tin, Tacc, OP, MAP>(acc[VEC - 1], p.x[i], HAS_Y ? p.y[i] : zero_of<Tin>());
 
   const char *xb = reinterpret_cast<const char *>(p.x + p.head);
   const char *yb = HAS_Y ? reinterpret_cast<const char *>(p.y + p.head) : nullptr;
@@ -154,7 +174,10 @@ __global__ void __launch_bounds__(RED_BLOCK, MINB) reduce_kernel(RedArgs<Tin, Ta
   constexpr bool FILL = OP == GA_OP_SUM || MAP == GA_MAP_ID;
   V32 fill;
 #pragma unroll
-  for (int k = 0; k < VEC; ++k) vset<Tin>(fill, k, OP == GA_OP_SUM ? Tin(0) : (Tin)Op<OP, Tacc>::neutral());
+  for (int k = 0; k < VEC; ++k) {
+    if constexpr (OP == GA_OP_SUM) vset<Tin>(fill, k, zero_of<Tin>());
+    else vset<Tin>(fill, k, (Tin)Op<OP, Tacc>::neutral());
+  }
   // One batch: UNROLL vectors per input, RED_BLOCK apart, all loaded before
   // any is used; out-of-range vectors take the neutral fill.
   auto batch = [&](int64_t base) {
@@ -175,7 +198,7 @@ __global__ void __launch_bounds__(RED_BLOCK, MINB) reduce_kernel(RedArgs<Tin, Ta
       if (FILL || base + j * RED_BLOCK < p.nvec) {
 #pragma unroll
         for (int k = 0; k < VEC; ++k)
-          acc[k] = map_acc<Tin, Tacc, OP, MAP>(acc[k], vget<Tin>(vx[j], k), HAS_Y ? vget<Tin>(vy[j], k) : Tin(0));
+          acc[k] = map_acc<Tin, Tacc, OP, MAP>(acc[k], vget<Tin>(vx[j], k), HAS_Y ? vget<Tin>(vy[j], k) : zero_of<Tin>());
       }
   };
   // The first batch is peeled out of the loop (the loop only runs when the
@@ -213,7 +236,7 @@ __global__ void __launch_bounds__(RED_BLOCK, MINB) reduce_kernel(RedArgs<Tin, Ta
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int i = base + j * RED_BLOCK;
-      v[j] = i < (int)gridDim.x ? __ldcg(p.partials + i) : Op<OP, Tacc>::neutral();
+      v[j] = i < (int)gridDim.x ? ldcg<Tacc>(p.partials + i) : Op<OP, Tacc>::neutral();
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) w = Op<OP, Tacc>::fold(w, v[j]);

@@ -105,8 +105,8 @@ size_t scan_workspace_bytes(ga_dtype_t dt, int64_t n) {
     case GA_I64: return ws_bytes<int64_t>(n);
     case GA_F32: return ws_bytes<float>(n);
     case GA_F64: return ws_bytes<double>(n);
+    default: return 0;
   }
-  return 0;
 }
 
 ga_status_t launch_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_t n, const void *in, void *out,
@@ -117,6 +117,7 @@ ga_status_t launch_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_t 
     case GA_I64: return by_op<int64_t>(op, ex, n, in, out, carry, carry_count, ws, s);
     case GA_F32: return by_op<float>(op, ex, n, in, out, carry, carry_count, ws, s);
     case GA_F64: return by_op<double>(op, ex, n, in, out, carry, carry_count, ws, s);
+    default: break;
   }
   return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad dtype %d", (int)dt);
 }

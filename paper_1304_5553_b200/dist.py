@@ -135,11 +135,13 @@ def reduce_fused(op, map_, x, y=None, out_dtype=None, out=None, exchange=None, p
     from . import _abi
     from . import gpuarray as G
     G._check_array("x", x)
-    if map_ == G.MUL:
+    has_y = map_ in (G.MUL, G.CONJ_MUL)
+    if has_y:
         if y is None:
-            raise ValueError("map MUL needs y")
+            raise ValueError("maps MUL / CONJ_MUL need y")
         G._same(x, y, "y")
-    out_dtype = x.dtype if out_dtype is None else out_dtype
+    if out_dtype is None:
+        out_dtype = G._REAL_OF.get(x.dtype, x.dtype) if map_ == G.SQUARE else x.dtype
     if out is None:
         out = torch.empty((), dtype=out_dtype, device=x.device)
     in_dt, out_dt = G.ga_dtype(x.dtype), G.ga_dtype(out_dtype)
@@ -148,7 +150,7 @@ def reduce_fused(op, map_, x, y=None, out_dtype=None, out=None, exchange=None, p
     w = G.workspace("reduce", x.device, s, nb)
     seq = exchange.next_seq()
     G.check(_abi.gpuarray_reduce_xgpu(op, map_, in_dt, out_dt, x.numel(), G._ptr(x),
-                                      G._ptr(y) if map_ == G.MUL else None, out.data_ptr(), w.data_ptr(), w.numel(),
+                                      G._ptr(y) if has_y else None, out.data_ptr(), w.data_ptr(), w.numel(),
                                       exchange.peers.data_ptr(), exchange.rank, exchange.world, seq,
                                       _abi.GA_XGPU_EXCLUSIVE_PREFIX if prefix_only else _abi.GA_XGPU_ALL, s))
     return out

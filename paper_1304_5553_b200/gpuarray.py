@@ -20,20 +20,23 @@ import builtins
 import torch
 
 from . import _abi
-from ._abi import (GA_F32, GA_F64, GA_I32, GA_I64, GA_MAP_ID, GA_MAP_MUL, GA_MAP_SQUARE, GA_OP_MAX, GA_OP_MIN,
-                   GA_OP_SUM, GA_SCAN_EXCLUSIVE, GA_SCAN_INCLUSIVE, check, make_scalar)
+from ._abi import (GA_C64, GA_C128, GA_F32, GA_F64, GA_I32, GA_I64, GA_MAP_CONJ_MUL, GA_MAP_ID, GA_MAP_MUL,
+                   GA_MAP_SQUARE, GA_OP_MAX, GA_OP_MIN, GA_OP_SUM, GA_SCAN_EXCLUSIVE, GA_SCAN_INCLUSIVE, check,
+                   make_scalar)
 
 SUM, MAX, MIN = GA_OP_SUM, GA_OP_MAX, GA_OP_MIN
-ID, MUL, SQUARE = GA_MAP_ID, GA_MAP_MUL, GA_MAP_SQUARE
+ID, MUL, SQUARE, CONJ_MUL = GA_MAP_ID, GA_MAP_MUL, GA_MAP_SQUARE, GA_MAP_CONJ_MUL
 
-_DT = {torch.float32: GA_F32, torch.float64: GA_F64, torch.int32: GA_I32, torch.int64: GA_I64}
+_DT = {torch.float32: GA_F32, torch.float64: GA_F64, torch.int32: GA_I32, torch.int64: GA_I64,
+       torch.complex64: GA_C64, torch.complex128: GA_C128}
+_REAL_OF = {torch.complex64: torch.float32, torch.complex128: torch.float64}
 
 
 def ga_dtype(t):
     try:
         return _DT[t]
     except KeyError:
-        raise TypeError(f"unsupported dtype {t}; expected float32/float64/int32/int64") from None
+        raise TypeError(f"unsupported dtype {t}; expected float32/float64/int32/int64/complex64/complex128") from None
 
 
 def _check_array(name, t):
@@ -120,11 +123,13 @@ def reduce(op, map_, x, y=None, out_dtype=None, out=None):
     """Fold map(x, y) with op from its neutral element; returns a 0-d device
     tensor of out_dtype (default: x.dtype)."""
     _check_array("x", x)
-    if map_ == MUL:
+    has_y = map_ in (MUL, CONJ_MUL)
+    if has_y:
         if y is None:
-            raise ValueError("map MUL needs y")
+            raise ValueError("maps MUL / CONJ_MUL need y")
         _same(x, y, "y")
-    out_dtype = x.dtype if out_dtype is None else out_dtype
+    if out_dtype is None:  # |x|^2 of complex data is real
+        out_dtype = _REAL_OF.get(x.dtype, x.dtype) if map_ == SQUARE else x.dtype
     if out is None:
         out = torch.empty((), dtype=out_dtype, device=x.device)
     elif out.numel() != 1 or out.dtype != out_dtype or out.device != x.device:
@@ -133,7 +138,7 @@ def reduce(op, map_, x, y=None, out_dtype=None, out=None):
     s = _stream(x)
     nb = _abi.gpuarray_reduce_workspace_bytes(out_dt, x.numel())
     w = workspace("reduce", x.device, s, nb)
-    check(_abi.gpuarray_reduce(op, map_, in_dt, out_dt, x.numel(), _ptr(x), _ptr(y) if map_ == MUL else None,
+    check(_abi.gpuarray_reduce(op, map_, in_dt, out_dt, x.numel(), _ptr(x), _ptr(y) if has_y else None,
                                out.data_ptr(), w.data_ptr(), w.numel(), s))
     return out
 
@@ -143,12 +148,18 @@ def dot(x, y, out_dtype=None, out=None):
     return reduce(SUM, MUL, x, y, out_dtype=out_dtype, out=out)
 
 
+def vdot(x, y, out=None):
+    """sum conj(x[i]) * y[i] (equal to dot for real data)."""
+    return reduce(SUM, CONJ_MUL, x, y, out=out)
+
+
 def sum(x, out_dtype=None, out=None):  # noqa: A001 - numpy-patterned name (PAPER.md:378-381)
     return reduce(SUM, ID, x, out_dtype=out_dtype, out=out)
 
 
 def norm2sq(x, out_dtype=None, out=None):
-    """Squared 2-norm: map x[i]*x[i], reduce a+b (x is read once)."""
+    """Squared 2-norm: map x[i]*x[i] (|x[i]|^2 for complex, into the real
+    type), reduce a+b (x is read once)."""
     return reduce(SUM, SQUARE, x, out_dtype=out_dtype, out=out)
 
 

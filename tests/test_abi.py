@@ -38,14 +38,15 @@ def test_nm_shows_c_linkage(abi):
 
 
 def test_version_and_strings(abi):
-    assert abi.gpuarray_abi_version() == 1
+    assert abi.gpuarray_abi_version() == 2
     assert abi.gpuarray_status_string(abi.GA_OK) == "GA_OK"
     assert abi.gpuarray_status_string(abi.GA_ERR_CUDA) == "GA_ERR_CUDA"
     assert abi.gpuarray_status_string(99) == "GA_ERR_UNKNOWN"
 
 
 def test_workspace_sizes(abi):
-    assert abi.gpuarray_reduce_workspace_bytes(abi.GA_F32, 1 << 30) >= 128 + 8 * 1184
+    assert abi.gpuarray_reduce_workspace_bytes(abi.GA_F32, 1 << 30) == 128 + 16 * 32768
+    assert abi.gpuarray_xgpu_buffer_bytes() == 2 * 64 * 32
     a = abi.gpuarray_scan_workspace_bytes(abi.GA_I32, 1 << 30)
     assert a == 256 + 8 * ((1 << 30) // 4096)
     b = abi.gpuarray_scan_workspace_bytes(abi.GA_I64, 1 << 20)
@@ -71,6 +72,9 @@ def test_argument_validation_is_synchronous(abi):
     R = abi.gpuarray_reduce
     assert R(5, 0, 0, 0, 4, 4096, None, 64, 128, ws, None) == E                                # bad op
     assert R(0, 5, 0, 0, 4, 4096, None, 64, 128, ws, None) == E                                # bad map
+    assert R(0, abi.GA_MAP_CONJ_MUL, 0, 0, 4, 4096, None, 64, 128, ws, None) == E              # CONJ_MUL without y
+    assert R(1, 0, abi.GA_C64, abi.GA_C64, 4, 4096, None, 64, 128, ws, None) == abi.GA_ERR_UNSUPPORTED  # max of complex
+    assert R(0, 2, abi.GA_C64, abi.GA_C64, 4, 4096, None, 64, 128, ws, None) == abi.GA_ERR_UNSUPPORTED  # |x|^2 -> real
     assert R(0, abi.GA_MAP_MUL, 0, 0, 4, 4096, None, 64, 128, ws, None) == E                   # MUL without y
     assert R(0, 0, 0, 0, 4, 4096, None, None, 128, ws, None) == E                              # no out
     assert R(0, 0, 0, 0, 4, 4096, None, 64, 128, ws - 1, None) == abi.GA_ERR_WORKSPACE
@@ -79,6 +83,7 @@ def test_argument_validation_is_synchronous(abi):
     sw = abi.gpuarray_scan_workspace_bytes(abi.GA_I32, 100)
     assert S(5, 0, abi.GA_I32, 100, 4096, 8192, None, 0, 64, sw, None) == E                    # bad op
     assert S(0, 0, 9, 100, 4096, 8192, None, 0, 64, sw, None) == E                            # bad dtype
+    assert S(0, 0, abi.GA_C64, 100, 4096, 8192, None, 0, 64, sw, None) == abi.GA_ERR_UNSUPPORTED  # complex scan
     assert S(0, 3, abi.GA_I32, 100, 4096, 8192, None, 0, 64, sw, None) == E                   # bad kind
     assert S(0, 0, abi.GA_I32, 100, 4096, 8192, None, 2, 64, sw, None) == E                   # carry NULL
     assert S(0, 0, abi.GA_I32, 100, 4096, 4100, None, 0, 64, sw, None) == E                   # partial overlap
@@ -103,5 +108,9 @@ def test_scalar_marshalling(abi):
     assert s.bits == 0xFFFFFFFF
     s = abi.make_scalar(abi.GA_I64, -2)
     assert s.bits == (1 << 64) - 2
+    s = abi.make_scalar(abi.GA_C64, 1.5 - 2j)
+    assert struct.unpack("<ff", struct.pack("<Q", s.bits)) == (1.5, -2.0) and s.bits_hi == 0
+    s = abi.make_scalar(abi.GA_C128, 0.25 + 4j)
+    assert struct.unpack("<dd", struct.pack("<QQ", s.bits, s.bits_hi)) == (0.25, 4.0)
     import ctypes
-    assert ctypes.sizeof(abi.ga_scalar_t) == 16
+    assert ctypes.sizeof(abi.ga_scalar_t) == 24

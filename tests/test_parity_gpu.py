@@ -404,3 +404,70 @@ def test_scan_float_sum_within_bound(dt, exclusive, n):
         got = G.scan(to_dev(x, offs), exclusive=exclusive).cpu().numpy().astype(np.float64)
         d = np.arange(n) / 2048.0 + 512
         assert np.all(np.abs(got - ref) <= d * u * sa + 1e-300)
+
+
+# ------------------------------------------------------------------ complex (NEXT-3)
+CPLX = {np.complex64: torch.complex64, np.complex128: torch.complex128}
+
+
+def cplx_data(dt, n, seed):
+    f = synth.F32_S11 if dt == np.complex64 else synth.F64_S11
+    return synth.host_fill(f, seed, 2 * n).view(dt)
+
+
+def to_dev_c(a, offset=0):
+    buf = torch.empty(a.size + offset, dtype=CPLX[a.dtype.type], device=DEV)
+    v = buf[offset:]
+    v.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+    return v
+
+
+@pytest.mark.parametrize("dt", [np.complex64, np.complex128])
+@pytest.mark.parametrize("n", [1, 3, 4097, 100_003])
+@pytest.mark.parametrize("offs", [0, 1])
+def test_complex_axpbyz_bit_exact(dt, n, offs):
+    x = cplx_data(dt, n, 1)
+    y = cplx_data(dt, n, 2)
+    a, b = 1.5 - 2.25j, -0.75 + 0.5j
+    z = ga.axpbyz(a, to_dev_c(x, offs), b, to_dev_c(y, offs)).cpu().numpy()
+    ref = oracle.axpbyz_complex(dt(a), x, dt(b), y)
+    f = np.float32 if dt == np.complex64 else np.float64
+    assert_bit_exact(z.view(f), ref.view(f))
+    # axpbz(a, x, b) == axpbyz(a, x, b, 1) on nonzero data
+    zb = ga.axpbz(a, to_dev_c(x), b).cpu().numpy()
+    assert_bit_exact(zb.view(f), oracle.axpbyz_complex(dt(a), x, dt(b), np.ones_like(x)).view(f))
+
+
+@pytest.mark.parametrize("dt", [np.complex64, np.complex128])
+@pytest.mark.parametrize("n", [1, 257, 100_003, 2_000_003])
+def test_complex_sum_dot_vdot_norm2(dt, n):
+    x = cplx_data(dt, n, 3)
+    y = cplx_data(dt, n, 4)
+    u, rel = (2.0 ** -24, 1e-5) if dt == np.complex64 else (2.0 ** -53, 1e-12)
+    xd, yd = to_dev_c(x), to_dev_c(y, 1)
+    for name, got, mp in (("sum", G.sum(xd), oracle.MAP_ID), ("dot", G.dot(xd, to_dev_c(y)), oracle.MAP_MUL),
+                          ("vdot", G.vdot(xd, to_dev_c(y)), oracle.MAP_CONJ_MUL)):
+        ref, sa = oracle.reduce_complex(mp, x, y, return_sumabs=True)
+        g = complex(got.item())
+        assert abs(g - ref) <= max(rel * abs(ref), 2 * n * u * sa), name
+    n2 = G.norm2sq(xd)
+    assert n2.dtype == (torch.float32 if dt == np.complex64 else torch.float64)
+    ref = oracle.reduce_complex(oracle.MAP_SQUARE, x)
+    assert abs(float(n2.item()) - ref) <= rel * ref
+    # unaligned y (offset 1 element) takes the scalar path
+    g = complex(G.vdot(xd, yd).item())
+    ref, sa = oracle.reduce_complex(oracle.MAP_CONJ_MUL, x, y, return_sumabs=True)
+    assert abs(g - ref) <= max(rel * abs(ref), 2 * n * u * sa)
+
+
+def test_complex_closed_forms_and_errors():
+    n = 1 << 20
+    ones = torch.ones(n, dtype=torch.complex64, device=DEV)
+    i_ = torch.full((n,), 1j, dtype=torch.complex64, device=DEV)
+    assert complex(G.dot(i_, i_).item()) == -n          # i*i = -1
+    assert complex(G.vdot(i_, i_).item()) == n          # conj(i)*i = 1
+    assert float(G.norm2sq(i_ + ones).item()) == 2 * n  # |1+i|^2 = 2
+    with pytest.raises(TypeError):
+        G.max(ones)
+    with pytest.raises(TypeError):
+        G.scan(ones)

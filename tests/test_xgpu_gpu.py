@@ -126,3 +126,22 @@ def test_fused_sharded_scan(world, exclusive):
         torch.cuda.synchronize()
         got = np.concatenate([o.cpu().numpy() for o in outs])
         assert np.array_equal(got, oracle.scan(oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE, kh))
+
+
+def test_fused_complex_vdot():
+    """16-byte (complex128) values through the exchange slots."""
+    world = 3
+    exchs = make_ranks(world)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    n = 300_001
+    xh = synth.host_fill(synth.F64_S11, 11, 2 * n).view(np.complex128)
+    yh = synth.host_fill(synth.F64_S11, 12, 2 * n).view(np.complex128)
+    spans = [gdist.shard_range(n, world, r) for r in range(world)]
+    shards = [(torch.from_numpy(xh[s:s + c]).to(DEV), torch.from_numpy(yh[s:s + c]).to(DEV)) for s, c in spans]
+    warm = torch.ones(64, dtype=torch.complex128, device=DEV)
+    G.vdot(warm, warm)
+    for rep in range(2):
+        outs = run_all(exchs, shards, G.SUM, G.CONJ_MUL, None, streams)
+        ref, sa = oracle.reduce_complex(oracle.MAP_CONJ_MUL, xh, yh, return_sumabs=True)
+        assert all(o.tobytes() == outs[0].tobytes() for o in outs)
+        assert abs(complex(outs[0]) - ref) <= max(1e-12 * abs(ref), 2 * n * 2.0 ** -53 * sa)
