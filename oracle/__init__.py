@@ -82,6 +82,10 @@ def lib():
         L.oracle_sum_complex.argtypes = [ctypes.c_int, ctypes.c_int, i64, vp, vp, vp, vp]
         L.oracle_norm2_complex.restype = d
         L.oracle_norm2_complex.argtypes = [ctypes.c_int, i64, vp]
+        L.oracle_stencil3_f64.restype = None
+        L.oracle_stencil3_f64.argtypes = [i64, d, d, d, vp, vp, vp]
+        L.oracle_stencil3_f32.restype = None
+        L.oracle_stencil3_f32.argtypes = [i64, f32, f32, f32, vp, vp, vp]
         L.oracle_scan_sum_float.restype = None
         L.oracle_scan_sum_float.argtypes = [ctypes.c_int, ctypes.c_int, i64, vp, vp, d, vp]
         _lib = L
@@ -223,3 +227,16 @@ def scan(kind, x, carry=None, out=None, op=SUM, return_sumabs=False):
     else:
         L.oracle_scan_maxmin_int(op, kind, _DT[x.dtype], x.size, _ptr(x), _ptr(out), int(c))
     return out
+
+
+def stencil3(l, d, u, x, diag=None):
+    """y_i = l*x_{i-1} + d_i*x_i + u*x_{i+1}, boundary terms omitted, each
+    step RN left to right (R25); d_i = diag[i] when diag is given."""
+    x = _c(x)
+    y = np.empty_like(x)
+    if diag is not None:
+        diag = _c(diag, x.dtype)
+    st = x.dtype.type
+    fn = lib().oracle_stencil3_f64 if x.dtype == np.float64 else lib().oracle_stencil3_f32
+    fn(x.size, st(l).item(), st(d).item(), st(u).item(), _ptr(diag) if diag is not None else None, _ptr(x), _ptr(y))
+    return y

@@ -435,3 +435,43 @@ double oracle_norm2_complex(int is_c128, int64_t n, const void *x) {
   }
   return acc.s + acc.c;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Three-point stencil / tridiagonal matvec for the CG workload (§8(f)       */
+/* NEXT-4; the paper's Krylov solver, applied matrix-free  */
+/* to 1-D Poisson-type systems).  y_i = l*x_{i-1} + d_i*x_i + u*x_{i+1} with */
+/* d_i = diag[i] if diag != NULL else d; the terms outside [0, n) are        */
+/* omitted (Dirichlet boundary), each operation one RN step, left to right:  */
+/*   y_i = RN(RN(RN(l*x_{i-1}) + RN(d_i*x_i)) + RN(u*x_{i+1}))   (R25)       */
+/* ------------------------------------------------------------------------ */
+void oracle_stencil3_f64(int64_t n, double l, double d, double u, const double *diag, const double *x, double *y) {
+  for (int64_t i = 0; i < n; ++i) {
+    double di = diag ? diag[i] : d;
+    double acc = di * x[i];
+    if (i > 0) {
+      double t = l * x[i - 1];
+      acc = t + acc;
+    }
+    if (i + 1 < n) {
+      double t = u * x[i + 1];
+      acc = acc + t;
+    }
+    y[i] = acc;
+  }
+}
+
+void oracle_stencil3_f32(int64_t n, float l, float d, float u, const float *diag, const float *x, float *y) {
+  for (int64_t i = 0; i < n; ++i) {
+    float di = diag ? diag[i] : d;
+    float acc = di * x[i];
+    if (i > 0) {
+      float t = l * x[i - 1];
+      acc = t + acc;
+    }
+    if (i + 1 < n) {
+      float t = u * x[i + 1];
+      acc = acc + t;
+    }
+    y[i] = acc;
+  }
+}

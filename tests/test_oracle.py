@@ -470,3 +470,39 @@ def test_complex_sums_against_fraction_and_fsum(dt):
     # vdot(x, x) = |x|^2 (imaginary part exactly 0)
     vv = oracle.reduce_complex(oracle.MAP_CONJ_MUL, x, x)
     assert vv.imag == 0.0 and vv.real == pytest.approx(oracle.reduce_complex(oracle.MAP_SQUARE, x), rel=1e-15)
+
+
+# ------------------------------------------------------------ stencil / tridiagonal matvec (NEXT-4)
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_stencil3_matches_dense_and_numpy(dt):
+    """Against numpy's uncontracted (l*x[:-2] + d*x[1:-1]) + u*x[2:] with the
+    boundary terms omitted, and against a dense tridiagonal matrix product
+    (float64, tolerance) — catches swapped l/u, a shifted neighbour, a
+    boundary term that should be omitted."""
+    n = 1001
+    x = synth.host_fill(synth.F32_S11 if dt == np.float32 else synth.F64_S11, 1, n)
+    l, d, u = dt(-1.25), dt(2.5), dt(-0.75)
+    y = oracle.stencil3(l, d, u, x)
+    ref = np.empty_like(x)
+    ref[1:-1] = ((l * x[:-2]) + (d * x[1:-1])) + (u * x[2:])
+    ref[0] = (d * x[0]) + (u * x[1])
+    ref[-1] = (l * x[-2]) + (d * x[-1])
+    assert bits_equal(y, ref)
+    A = np.diag(np.full(n, float(d))) + np.diag(np.full(n - 1, float(l)), -1) + np.diag(np.full(n - 1, float(u)), 1)
+    assert np.allclose(A @ x.astype(np.float64), y, rtol=0, atol=1e-5 if dt == np.float32 else 1e-13)
+    diag = synth.host_fill(synth.F32_U01 if dt == np.float32 else synth.F64_U01, 2, n)
+    yd = oracle.stencil3(l, d, u, x, diag=diag)
+    A = np.diag(diag.astype(np.float64)) + np.diag(np.full(n - 1, float(l)), -1) + np.diag(np.full(n - 1, float(u)), 1)
+    assert np.allclose(A @ x.astype(np.float64), yd, rtol=0, atol=1e-5 if dt == np.float32 else 1e-13)
+
+
+def test_stencil3_poisson_closed_forms():
+    """1-D Poisson (l = u = -1, d = 2): a constant vector maps to zero inside
+    and to the constant at the two ends; a linear ramp maps to zero inside."""
+    n = 100
+    c = np.full(n, 3.0)
+    y = oracle.stencil3(-1, 2, -1, c)
+    assert np.all(y[1:-1] == 0) and y[0] == 3.0 and y[-1] == 3.0
+    r = np.arange(n, dtype=np.float64)
+    y = oracle.stencil3(-1, 2, -1, r)
+    assert np.all(y[1:-1] == 0) and y[0] == -1.0 and y[-1] == n
