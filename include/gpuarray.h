@@ -178,6 +178,17 @@ ga_status_t gpuarray_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_
                           void *out, const void *carry, int64_t carry_count, void *workspace,
                           size_t workspace_bytes, void *stream);
 
+/* ---- Operator of the CG workload (the paper's
+ * "conjugate-gradient-based Krylov solver", applied
+ * matrix-free).  Three-point stencil / tridiagonal matvec, dt in {F32, F64}:
+ *   y[i] = l*x[i-1] + d_i*x[i] + u*x[i+1],  d_i = diag[i] if diag else d,
+ * terms outside [0, n) omitted (Dirichlet boundary), every operation RN left
+ * to right, no FMA (R25) — bit-exact against the oracle.  diag is
+ * an optional DEVICE array of n elements; y must not overlap x or diag.
+ * 1-D Poisson: l = u = -1, d = 2. */
+ga_status_t gpuarray_stencil3(ga_dtype_t dt, int64_t n, ga_scalar_t l, ga_scalar_t d, ga_scalar_t u,
+                              const void *diag, const void *x, void *y, void *stream);
+
 /* Static strings; never NULL. */
 const char *gpuarray_status_string(ga_status_t status);
 /* Thread-local detail of the last non-OK status on this thread ("" if none). */

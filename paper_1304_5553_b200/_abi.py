@@ -22,6 +22,7 @@ EXPORTS = (
     "gpuarray_axpbyz", "gpuarray_axpbz", "gpuarray_reduce_workspace_bytes", "gpuarray_reduce",
     "gpuarray_scan_workspace_bytes", "gpuarray_scan", "gpuarray_status_string", "gpuarray_last_error",
     "gpuarray_abi_version", "gpuarray_launch_count", "gpuarray_xgpu_buffer_bytes", "gpuarray_reduce_xgpu",
+    "gpuarray_stencil3",
 )
 
 
@@ -99,6 +100,8 @@ def _load():
     lib.gpuarray_reduce_xgpu.restype = st
     lib.gpuarray_reduce_xgpu.argtypes = [st, st, st, st, i64, vp, vp, vp, vp, sz, vp, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_uint64, st, vp]
+    lib.gpuarray_stencil3.restype = st
+    lib.gpuarray_stencil3.argtypes = [st, i64, ga_scalar_t, ga_scalar_t, ga_scalar_t, vp, vp, vp, vp]
     return lib
 
 
@@ -144,6 +147,10 @@ def gpuarray_scan_workspace_bytes(dt, n):
 
 def gpuarray_scan(op, kind, dt, n, in_, out, carry, carry_count, workspace, workspace_bytes, stream):
     return LIB.gpuarray_scan(op, kind, dt, n, in_, out, carry, carry_count, workspace, workspace_bytes, stream)
+
+
+def gpuarray_stencil3(dt, n, l, d, u, diag, x, y, stream):
+    return LIB.gpuarray_stencil3(dt, n, l, d, u, diag, x, y, stream)
 
 
 def gpuarray_status_string(status):

@@ -59,6 +59,9 @@ ga_status_t launch_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t
 ga_status_t launch_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_t n, const void *in, void *out,
                         const void *carry, int64_t carry_count, void *ws, cudaStream_t s);
 
+ga_status_t launch_stencil3(ga_dtype_t dt, int64_t n, const ga_scalar_t &l, const ga_scalar_t &d,
+                            const ga_scalar_t &u, const void *diag, const void *x, void *y, cudaStream_t s);
+
 size_t reduce_workspace_bytes();
 size_t scan_workspace_bytes(ga_dtype_t dt, int64_t n);
 

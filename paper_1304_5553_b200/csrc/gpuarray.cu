@@ -171,6 +171,22 @@ ga_status_t gpuarray_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_
   return launch_scan(op, kind, dt, n, in, out, carry, carry_count, workspace, (cudaStream_t)stream);
 }
 
+ga_status_t gpuarray_stencil3(ga_dtype_t dt, int64_t n, ga_scalar_t l, ga_scalar_t d, ga_scalar_t u,
+                              const void *diag, const void *x, void *y, void *stream) {
+  if (!valid_dtype(dt)) return fail(GA_ERR_INVALID_ARGUMENT, "stencil3: bad dtype %d", (int)dt);
+  if (n < 0) return fail(GA_ERR_INVALID_ARGUMENT, "stencil3: n < 0");
+  if (!scalar_ok(l, dt) || !scalar_ok(d, dt) || !scalar_ok(u, dt))
+    return fail(GA_ERR_INVALID_ARGUMENT, "stencil3: scalar dtype differs from array dtype");
+  if (n == 0) return GA_OK;
+  if (!x || !y) return fail(GA_ERR_INVALID_ARGUMENT, "stencil3: NULL array with n > 0");
+  const size_t bytes = (size_t)n * dtype_size(dt);
+  if ((uintptr_t)x < (uintptr_t)y + bytes && (uintptr_t)y < (uintptr_t)x + bytes)
+    return fail(GA_ERR_INVALID_ARGUMENT, "stencil3: y overlaps x (neighbours are read)");
+  if (diag && (uintptr_t)diag < (uintptr_t)y + bytes && (uintptr_t)y < (uintptr_t)diag + bytes)
+    return fail(GA_ERR_INVALID_ARGUMENT, "stencil3: y overlaps diag");
+  return launch_stencil3(dt, n, l, d, u, diag, x, y, (cudaStream_t)stream);
+}
+
 const char *gpuarray_status_string(ga_status_t s) {
   switch (s) {
     case GA_OK: return "GA_OK";

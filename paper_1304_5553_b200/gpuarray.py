@@ -118,6 +118,23 @@ def axpbz(a, x, b, out=None):
     return out
 
 
+def stencil3(l, d, u, x, diag=None, out=None):
+    """y[i] = l*x[i-1] + d_i*x[i] + u*x[i+1] (boundary terms omitted, every
+    step RN, R25); d_i = diag[i] when a diagonal array is given.  The
+    operator of the CG workload."""
+    _check_array("x", x)
+    if out is None:
+        out = torch.empty_like(x)
+    else:
+        _same(x, out, "out")
+    if diag is not None:
+        _same(x, diag, "diag")
+    dt = ga_dtype(x.dtype)
+    check(_abi.gpuarray_stencil3(dt, x.numel(), make_scalar(dt, l), make_scalar(dt, d), make_scalar(dt, u),
+                                 _ptr(diag) if diag is not None else None, _ptr(x), _ptr(out), _stream(x)))
+    return out
+
+
 # --------------------------------------------------------------- map-reduce
 def reduce(op, map_, x, y=None, out_dtype=None, out=None):
     """Fold map(x, y) with op from its neutral element; returns a 0-d device
