@@ -96,6 +96,23 @@ typedef struct ga_scalar {
 ga_status_t gpuarray_axpbyz(ga_dtype_t dt, int64_t n, ga_scalar_t a, const void *x, ga_scalar_t b,
                             const void *y, void *z, void *stream);
 
+/* A coefficient that may live on the GPU (a reduction's
+ * GPUArray scalar "used in-place on the GPU"): value = scale when num and
+ * den are both NULL, else RN(scale * RN(num / den)) with a NULL pointer
+ * standing for 1 and a zero numerator giving 0 whatever den (0/0 -> 0).  num / den are DEVICE scalars of the call's dt, read when
+ * the kernel runs — so a chain of calls (e.g. a CG iteration) needs no host
+ * round trip and can be captured in a CUDA graph. */
+typedef struct ga_dscalar {
+  ga_scalar_t scale;
+  const void *num;
+  const void *den;
+} ga_dscalar_t;
+
+/* axpbyz with device-resident coefficient factors; dt in {F32, F64}; same
+ * rounding sequence, overlap rules and n == 0 behaviour as gpuarray_axpbyz. */
+ga_status_t gpuarray_axpbyz_ds(ga_dtype_t dt, int64_t n, ga_dscalar_t a, const void *x, ga_dscalar_t b,
+                               const void *y, void *z, void *stream);
+
 /* z[i] = a*x[i] + b (floats: RN(RN(a*x_i) + b)).  Listing 1's "multiply by
  * two" is a = 2, b = -0.0 (the IEEE additive identity, R21). */
 ga_status_t gpuarray_axpbz(ga_dtype_t dt, int64_t n, ga_scalar_t a, const void *x, ga_scalar_t b,

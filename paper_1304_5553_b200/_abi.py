@@ -22,7 +22,7 @@ EXPORTS = (
     "gpuarray_axpbyz", "gpuarray_axpbz", "gpuarray_reduce_workspace_bytes", "gpuarray_reduce",
     "gpuarray_scan_workspace_bytes", "gpuarray_scan", "gpuarray_status_string", "gpuarray_last_error",
     "gpuarray_abi_version", "gpuarray_launch_count", "gpuarray_xgpu_buffer_bytes", "gpuarray_reduce_xgpu",
-    "gpuarray_stencil3",
+    "gpuarray_stencil3", "gpuarray_axpbyz_ds",
 )
 
 
@@ -33,6 +33,19 @@ class ga_scalar_t(ctypes.Structure):
     ctypes cannot pass unions by value portably."""
     _fields_ = [("dtype", ctypes.c_int32), ("reserved", ctypes.c_int32), ("bits", ctypes.c_uint64),
                 ("bits_hi", ctypes.c_uint64)]
+
+
+class ga_dscalar_t(ctypes.Structure):
+    """{ga_scalar_t scale; const void *num; const void *den} (40 bytes)."""
+    _fields_ = [("scale", ga_scalar_t), ("num", ctypes.c_void_p), ("den", ctypes.c_void_p)]
+
+
+def make_dscalar(dt, scale, num=None, den=None):
+    d = ga_dscalar_t()
+    d.scale = make_scalar(dt, scale)
+    d.num = num
+    d.den = den
+    return d
 
 
 def make_scalar(dt, value):
@@ -100,6 +113,8 @@ def _load():
     lib.gpuarray_reduce_xgpu.restype = st
     lib.gpuarray_reduce_xgpu.argtypes = [st, st, st, st, i64, vp, vp, vp, vp, sz, vp, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_uint64, st, vp]
+    lib.gpuarray_axpbyz_ds.restype = st
+    lib.gpuarray_axpbyz_ds.argtypes = [st, i64, ga_dscalar_t, vp, ga_dscalar_t, vp, vp, vp]
     lib.gpuarray_stencil3.restype = st
     lib.gpuarray_stencil3.argtypes = [st, i64, ga_scalar_t, ga_scalar_t, ga_scalar_t, vp, vp, vp, vp]
     return lib
@@ -147,6 +162,10 @@ def gpuarray_scan_workspace_bytes(dt, n):
 
 def gpuarray_scan(op, kind, dt, n, in_, out, carry, carry_count, workspace, workspace_bytes, stream):
     return LIB.gpuarray_scan(op, kind, dt, n, in_, out, carry, carry_count, workspace, workspace_bytes, stream)
+
+
+def gpuarray_axpbyz_ds(dt, n, a, x, b, y, z, stream):
+    return LIB.gpuarray_axpbyz_ds(dt, n, a, x, b, y, z, stream)
 
 
 def gpuarray_stencil3(dt, n, l, d, u, diag, x, y, stream):

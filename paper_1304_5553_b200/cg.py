@@ -57,3 +57,88 @@ def cg(b, offdiag=-1.0, d=2.0, diag=None, x0=None, rtol=1e-10, maxiter=None):
         k += 1
         hist.append(math.sqrt(rs))
     return CGResult(x, k, hist, math.sqrt(rs) <= rtol * bnorm)
+
+
+class GraphCG:
+    """CG with every scalar left on the GPU: alpha = rs/pAp and beta =
+    rs_new/rs enter the axpbyz kernels as device-resident factors
+    (gpuarray_axpbyz_ds), so `block` iterations (an even number) are captured
+    ONCE in a CUDA graph at construction and replayed by every solve(); the
+    host reads the residual only between blocks.  Iteration counts are
+    rounded up to whole blocks (a zero numerator keeps a converged iteration
+    finite, see ga_dscalar_t)."""
+
+    def __init__(self, n, dtype=torch.float64, offdiag=-1.0, d=2.0, diag=None, block=16, device=None):
+        if block < 2 or block % 2:
+            raise ValueError("block must be an even number >= 2")
+        if dtype not in (torch.float32, torch.float64):
+            raise TypeError("GraphCG needs float32 or float64")
+        dev = torch.device(device or "cuda")
+        self.n, self.block, self.dev = n, block, dev
+        self.offdiag, self.d, self.diag = offdiag, d, diag
+        mk = lambda: torch.zeros(n, dtype=dtype, device=dev)  # noqa: E731
+        self.b, self.x, self.r, self.p, self.ap = mk(), mk(), mk(), mk(), mk()
+        self.rs = [torch.zeros(1, dtype=dtype, device=dev) for _ in range(2)]
+        self.pap = torch.zeros(1, dtype=dtype, device=dev)
+        self.stream = torch.cuda.Stream(dev)
+        self.stream.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(self.stream):  # warm-up: module loading, workspaces
+            self.b.fill_(1.0)
+            self._start()
+            for k in range(block):
+                self._iteration(k)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            for k in range(block):
+                self._iteration(k)
+
+    def _start(self):
+        G.stencil3(self.offdiag, self.d, self.offdiag, self.x, diag=self.diag, out=self.ap)
+        G.axpbyz(1.0, self.b, -1.0, self.ap, out=self.r)
+        G.axpbz(1.0, self.r, -0.0, out=self.p)
+        G.reduce(G.SUM, G.SQUARE, self.r, out=self.rs[0])
+
+    def _iteration(self, k):
+        cur, nxt = self.rs[k & 1], self.rs[(k + 1) & 1]
+        x, r, p, ap, pap = self.x, self.r, self.p, self.ap, self.pap
+        G.stencil3(self.offdiag, self.d, self.offdiag, p, diag=self.diag, out=ap)
+        G.reduce(G.SUM, G.MUL, p, ap, out=pap)
+        G.axpbyz_ds(1.0, x, 1.0, p, out=x, b_num=cur, b_den=pap)      # x += (rs/pAp) p
+        G.axpbyz_ds(1.0, r, -1.0, ap, out=r, b_num=cur, b_den=pap)    # r -= (rs/pAp) Ap
+        G.reduce(G.SUM, G.SQUARE, r, out=nxt)                          # rs_new
+        G.axpbyz_ds(1.0, r, 1.0, p, out=p, b_num=nxt, b_den=cur)      # p = r + (rs_new/rs) p
+
+    def solve(self, b, x0=None, rtol=1e-10, maxiter=None):
+        G._check_array("b", b)
+        if b.numel() != self.n or b.dtype != self.b.dtype:
+            raise ValueError("b does not match the solver's size / dtype")
+        maxiter = self.n if maxiter is None else maxiter
+        s = self.stream
+        s.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(s):
+            self.b.copy_(b)
+            if x0 is None:
+                self.x.zero_()
+            else:
+                self.x.copy_(x0)
+            self._start()
+            bnorm = math.sqrt(float(G.norm2sq(self.b).item()))
+            res = math.sqrt(float(self.rs[0].item()))
+        hist = [res]
+        k, conv = 0, res <= rtol * bnorm
+        while not conv and k < maxiter:
+            self.graph.replay()
+            k += self.block
+            res = math.sqrt(float(self.rs[0].item()))  # block is even: rs[0] holds the latest
+            hist.append(res)
+            conv = res <= rtol * bnorm
+        torch.cuda.current_stream(self.dev).wait_stream(s)
+        return CGResult(self.x.clone(), k, hist, conv)
+
+
+def cg_graph(b, offdiag=-1.0, d=2.0, diag=None, x0=None, rtol=1e-10, maxiter=None, block=16):
+    """One-shot convenience wrapper around GraphCG (captures a graph per call;
+    build a GraphCG once to solve repeatedly)."""
+    solver = GraphCG(b.numel(), b.dtype, offdiag, d, diag, block, b.device)
+    return solver.solve(b, x0=x0, rtol=rtol, maxiter=maxiter)

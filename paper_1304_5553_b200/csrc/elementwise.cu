@@ -37,7 +37,24 @@ struct EwArgs {
   const T *x;
   const T *y;  // unused by axpbz
   T *z;
+  // device-resident scalar factors (gpuarray_axpbyz_ds): a = RN(a * RN(an / ad)),
+  // a missing pointer standing for 1; all NULL: a and b as given
+  const T *an = nullptr, *ad = nullptr, *bn = nullptr, *bd = nullptr;
 };
+
+template <typename T>
+__device__ __forceinline__ T coef(T scale, const T *num, const T *den) {
+  if constexpr (std::is_floating_point<T>::value) {
+    if (!num && !den) return scale;
+    const T nv = num ? *num : T(1);
+    // a zero numerator gives a zero factor whatever the denominator (a
+    // converged CG iteration has 0/0 and must stay finite)
+    const T q = nv == T(0) ? T(0) : (den ? e_div(nv, *den) : nv);
+    return e_mul(scale, q);
+  } else {
+    return scale;
+  }
+}
 
 // One element of the statement; the rounding sequence is DESIGN.md R1.
 template <typename T, bool HAS_Y>
@@ -50,6 +67,8 @@ template <typename T, bool HAS_Y, int UNROLL, bool NC>
 __global__ void __launch_bounds__(EW_BLOCK) ew_vec_kernel(EwArgs<T> p) {
   constexpr int VEC = 32 / sizeof(T);
   const int64_t tid = (int64_t)blockIdx.x * EW_BLOCK + threadIdx.x;
+  p.a = coef(p.a, p.an, p.ad);
+  p.b = coef(p.b, p.bn, p.bd);
 
   // Scalar head (to 32 B alignment) and tail (remainder of the body).
   const int64_t tail0 = p.head + p.nvec * VEC;
@@ -100,6 +119,8 @@ __global__ void __launch_bounds__(EW_BLOCK) ew_vec_kernel(EwArgs<T> p) {
 template <typename T, bool HAS_Y>
 __global__ void __launch_bounds__(EW_BLOCK) ew_scalar_kernel(EwArgs<T> p) {
   const int64_t nthreads = (int64_t)gridDim.x * EW_BLOCK;
+  p.a = coef(p.a, p.an, p.ad);
+  p.b = coef(p.b, p.bn, p.bd);
   for (int64_t i = (int64_t)blockIdx.x * EW_BLOCK + threadIdx.x; i < p.n; i += nthreads) {
     T y = HAS_Y ? p.y[i] : zero_of<T>();
     p.z[i] = stmt<T, HAS_Y>(p.a, p.x[i], p.b, y);
@@ -123,7 +144,8 @@ c128 scalar_value<c128>(const ga_scalar_t &s) { return c128{s.v.c128[0], s.v.c12
 
 template <typename T, bool HAS_Y>
 ga_status_t launch_ew(int64_t n, const ga_scalar_t &a, const void *x, const ga_scalar_t &b, const void *y,
-                      void *z, cudaStream_t s) {
+                      void *z, cudaStream_t s, const void *an = nullptr, const void *ad = nullptr,
+                      const void *bn = nullptr, const void *bd = nullptr) {
   constexpr int VEC = 32 / sizeof(T);
   constexpr int UNROLL = HAS_Y ? 2 : 4;
   constexpr int64_t CHUNK = (int64_t)EW_BLOCK * UNROLL;
@@ -134,6 +156,10 @@ ga_status_t launch_ew(int64_t n, const ga_scalar_t &a, const void *x, const ga_s
   p.x = static_cast<const T *>(x);
   p.y = static_cast<const T *>(y);
   p.z = static_cast<T *>(z);
+  p.an = static_cast<const T *>(an);
+  p.ad = static_cast<const T *>(ad);
+  p.bn = static_cast<const T *>(bn);
+  p.bd = static_cast<const T *>(bd);
 
   const uintptr_t phase = (uintptr_t)x & 31;
   const bool coaligned = ((uintptr_t)z & 31) == phase && (!HAS_Y || ((uintptr_t)y & 31) == phase) &&
@@ -172,6 +198,14 @@ ga_status_t launch_axpbyz(ga_dtype_t dt, int64_t n, const ga_scalar_t &a, const 
     case GA_C128: return launch_ew<c128, true>(n, a, x, b, y, z, s);
   }
   return fail(GA_ERR_INVALID_ARGUMENT, "bad dtype %d", (int)dt);
+}
+
+ga_status_t launch_axpbyz_ds(ga_dtype_t dt, int64_t n, const ga_scalar_t &a, const void *an, const void *ad,
+                             const void *x, const ga_scalar_t &b, const void *bn, const void *bd, const void *y,
+                             void *z, cudaStream_t s) {
+  if (dt == GA_F32) return launch_ew<float, true>(n, a, x, b, y, z, s, an, ad, bn, bd);
+  if (dt == GA_F64) return launch_ew<double, true>(n, a, x, b, y, z, s, an, ad, bn, bd);
+  return fail(GA_ERR_UNSUPPORTED, "axpbyz_ds: device-scalar factors need F32 or F64");
 }
 
 ga_status_t launch_axpbz(ga_dtype_t dt, int64_t n, const ga_scalar_t &a, const void *x, const ga_scalar_t &b,

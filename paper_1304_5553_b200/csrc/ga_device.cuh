@@ -138,6 +138,8 @@ __device__ __forceinline__ int32_t e_add(int32_t a, int32_t b) { return (int32_t
 __device__ __forceinline__ int64_t e_add(int64_t a, int64_t b) { return (int64_t)((uint64_t)a + (uint64_t)b); }
 __device__ __forceinline__ int32_t e_sub(int32_t a, int32_t b) { return (int32_t)((uint32_t)a - (uint32_t)b); }
 __device__ __forceinline__ int64_t e_sub(int64_t a, int64_t b) { return (int64_t)((uint64_t)a - (uint64_t)b); }
+__device__ __forceinline__ float e_div(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double e_div(double a, double b) { return __ddiv_rn(a, b); }
 // Complex (R24): the product written out component-wise, every operation RN:
 // re(u*v) = RN(RN(ur*vr) - RN(ui*vi)), im(u*v) = RN(RN(ur*vi) + RN(ui*vr)).
 __device__ __forceinline__ c64 e_mul(c64 u, c64 v) {

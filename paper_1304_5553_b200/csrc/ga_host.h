@@ -52,6 +52,9 @@ struct Exchange {
 // Launchers implemented per kernel family (elementwise.cu, reduce.cu, scan.cu).
 ga_status_t launch_axpbyz(ga_dtype_t dt, int64_t n, const ga_scalar_t &a, const void *x,
                           const ga_scalar_t &b, const void *y, void *z, cudaStream_t s);
+ga_status_t launch_axpbyz_ds(ga_dtype_t dt, int64_t n, const ga_scalar_t &a, const void *an, const void *ad,
+                             const void *x, const ga_scalar_t &b, const void *bn, const void *bd, const void *y,
+                             void *z, cudaStream_t s);
 ga_status_t launch_axpbz(ga_dtype_t dt, int64_t n, const ga_scalar_t &a, const void *x,
                          const ga_scalar_t &b, void *z, cudaStream_t s);
 ga_status_t launch_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,

@@ -84,6 +84,22 @@ ga_status_t gpuarray_axpbyz(ga_dtype_t dt, int64_t n, ga_scalar_t a, const void 
   return launch_axpbyz(dt, n, a, x, b, y, z, (cudaStream_t)stream);
 }
 
+ga_status_t gpuarray_axpbyz_ds(ga_dtype_t dt, int64_t n, ga_dscalar_t a, const void *x, ga_dscalar_t b,
+                               const void *y, void *z, void *stream) {
+  if (!valid_dtype(dt)) return fail(GA_ERR_INVALID_ARGUMENT, "axpbyz_ds: bad dtype %d", (int)dt);
+  if (n < 0) return fail(GA_ERR_INVALID_ARGUMENT, "axpbyz_ds: n < 0");
+  if (!scalar_ok(a.scale, dt) || !scalar_ok(b.scale, dt))
+    return fail(GA_ERR_INVALID_ARGUMENT, "axpbyz_ds: scalar dtype differs from array dtype");
+  if (dt != GA_F32 && dt != GA_F64)
+    return fail(GA_ERR_UNSUPPORTED, "axpbyz_ds: device-scalar factors need F32 or F64");
+  if (n == 0) return GA_OK;
+  if (!x || !y || !z) return fail(GA_ERR_INVALID_ARGUMENT, "axpbyz_ds: NULL array with n > 0");
+  const size_t bytes = (size_t)n * dtype_size(dt);
+  if (partial_overlap(z, bytes, x, bytes) || partial_overlap(z, bytes, y, bytes))
+    return fail(GA_ERR_INVALID_ARGUMENT, "axpbyz_ds: z partially overlaps x or y");
+  return launch_axpbyz_ds(dt, n, a.scale, a.num, a.den, x, b.scale, b.num, b.den, y, z, (cudaStream_t)stream);
+}
+
 ga_status_t gpuarray_axpbz(ga_dtype_t dt, int64_t n, ga_scalar_t a, const void *x, ga_scalar_t b, void *z,
                            void *stream) {
   if (!valid_dtype(dt)) return fail(GA_ERR_INVALID_ARGUMENT, "axpbz: bad dtype %d", (int)dt);

@@ -105,6 +105,30 @@ def axpbyz(a, x, b, y, out=None):
     return out
 
 
+def axpbyz_ds(a, x, b, y, out=None, a_num=None, a_den=None, b_num=None, b_den=None):
+    """axpbyz whose coefficients may carry device-resident factors: the
+    effective a is RN(a * RN(a_num / a_den)) (missing tensor = 1), read when
+    the kernel runs (float32/float64; the factors are 1-element tensors of
+    x's dtype, e.g. reduction results left on the GPU)."""
+    _check_array("x", x)
+    _same(x, y, "y")
+    if out is None:
+        out = torch.empty_like(x)
+    else:
+        _same(x, out, "out")
+    dt = ga_dtype(x.dtype)
+
+    def ptr(t):
+        if t is None:
+            return None
+        if t.numel() != 1 or t.dtype != x.dtype or t.device != x.device:
+            raise ValueError("device scalar factors must be 1-element tensors of x's dtype and device")
+        return t.data_ptr()
+    check(_abi.gpuarray_axpbyz_ds(dt, x.numel(), _abi.make_dscalar(dt, a, ptr(a_num), ptr(a_den)), _ptr(x),
+                                  _abi.make_dscalar(dt, b, ptr(b_num), ptr(b_den)), _ptr(y), _ptr(out), _stream(x)))
+    return out
+
+
 def axpbz(a, x, b, out=None):
     """z = a*x + b in one pass (RN(RN(a*x)+b))."""
     _check_array("x", x)

@@ -93,3 +93,42 @@ def test_cg_large_consistency(dt, with_diag):
     bn = np.linalg.norm(bh.astype(np.float64))
     assert np.linalg.norm(r) <= rtol * bn + 50 * u * bn
     assert abs(np.linalg.norm(r) - res.residual_norms[-1]) <= 50 * u * bn + 0.5 * np.linalg.norm(r)
+
+
+def test_axpbyz_ds_bit_exact():
+    """Device-resident factors: a = RN(scale * RN(num / den)); 0/0 -> 0."""
+    n = 100_003
+    for dt, tdt in ((np.float32, torch.float32), (np.float64, torch.float64)):
+        x = synth.host_fill(synth.F32_S11 if dt == np.float32 else synth.F64_S11, 1, n)
+        y = synth.host_fill(synth.F32_S11 if dt == np.float32 else synth.F64_S11, 2, n)
+        num = torch.tensor([3.3], dtype=tdt, device=DEV)
+        den = torch.tensor([-0.7], dtype=tdt, device=DEV)
+        got = G.axpbyz_ds(1.5, to_dev(x), -2.0, to_dev(y), a_num=num, b_num=num, b_den=den).cpu().numpy()
+        a = dt(dt(1.5) * dt(3.3))
+        b = dt(dt(-2.0) * dt(dt(3.3) / dt(-0.7)))
+        assert np.array_equal(bits(got), bits(oracle.axpbyz(a, x, b, y)))
+        zero = torch.zeros(1, dtype=tdt, device=DEV)
+        got = G.axpbyz_ds(1.0, to_dev(x), 5.0, to_dev(y), b_num=zero, b_den=zero).cpu().numpy()
+        assert np.array_equal(bits(got), bits(oracle.axpbyz(dt(1), x, dt(0), y)))
+
+
+def test_cg_graph_matches_host_cg_f64():
+    """float64: the device-scalar iteration computes the same alpha/beta bits
+    as the host one (RN(rs/pAp) either way), so x and the residuals agree
+    exactly over the same number of iterations."""
+    n = 1 << 16
+    b = torch.from_numpy(synth.host_fill(synth.F64_S11, 7, n)).to(DEV)
+    ref = gcg.cg(b, offdiag=-1.0, d=4.0, rtol=0.0, maxiter=32)
+    got = gcg.cg_graph(b, offdiag=-1.0, d=4.0, rtol=0.0, maxiter=32, block=16)
+    assert got.iterations == ref.iterations == 32
+    assert torch.equal(got.x, ref.x)
+    assert got.residual_norms[-1] == ref.residual_norms[-1]
+
+
+def test_cg_graph_converges_poisson():
+    n = 64
+    b = torch.ones(n, dtype=torch.float64, device=DEV)
+    res = gcg.cg_graph(b, rtol=1e-10, block=8)
+    assert res.converged and res.iterations <= 72
+    A = 2 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)
+    assert np.allclose(res.x.cpu().numpy(), np.linalg.solve(A, np.ones(n)), rtol=1e-8, atol=0)

@@ -123,6 +123,15 @@ static int run_pipe(int64_t n, const void *in, void *out, void *ws, cudaStream_t
   X(146, int32_t, 16, 16, 4, 4, 1)           \
   X(147, int32_t, 16, 64, 8, 4, 1)           \
   X(148, int32_t, 16, 32, 8, 4, 0)           \
+  X(250, int32_t, 12, 32, 8, 8, 4)           \
+  X(251, int32_t, 12, 48, 8, 8, 4)           \
+  X(252, int32_t, 12, 64, 8, 8, 4)           \
+  X(253, int32_t, 16, 32, 8, 8, 5)           \
+  X(254, int32_t, 16, 48, 8, 8, 5)           \
+  X(255, int32_t, 8, 64, 8, 8, 4)            \
+  X(256, int32_t, 12, 40, 8, 8, 4)           \
+  X(257, int64_t, 12, 32, 8, 8, 4)           \
+  X(258, int64_t, 12, 48, 8, 8, 4)           \
   X(240, int32_t, 16, 32, 8, 4, 5)           \
   X(241, int32_t, 16, 32, 4, 4, 5)           \
   X(242, int32_t, 32, 16, 4, 4, 4)           \
@@ -297,4 +306,4 @@ extern "C" int64_t lab_scan_tile(int v) {
   return 0;
 }
 
-extern "C" int lab_scan_elem_bytes(int v) { return (v >= 20 && v < 40) || (v >= 60 && v < 78) || (v >= 90 && v < 100) || (v >= 120 && v < 140) || (v >= 160 && v < 170) || (v >= 178 && v < 180) || (v >= 191 && v < 200) || (v >= 220 && v < 230) || v == 235 || v == 236 || v == 248 || v == 249 ? 8 : 4; }
+extern "C" int lab_scan_elem_bytes(int v) { return (v >= 20 && v < 40) || (v >= 60 && v < 78) || (v >= 90 && v < 100) || (v >= 120 && v < 140) || (v >= 160 && v < 170) || (v >= 178 && v < 180) || (v >= 191 && v < 200) || (v >= 220 && v < 230) || v == 235 || v == 236 || v == 248 || v == 249 || v == 257 || v == 258 ? 8 : 4; }
