@@ -63,12 +63,17 @@ __device__ __forceinline__ T stmt(T a, T x, T b, T y) {
   else return e_add(e_mul(a, x), b);
 }
 
-template <typename T, bool HAS_Y, int UNROLL, bool NC>
+// DS: the coefficients carry device-resident factors (gpuarray_axpbyz_ds);
+// kept out of the plain instantiations, whose SASS must show only the R1
+// sequence (the IEEE division behind the factors is itself FMA-based).
+template <typename T, bool HAS_Y, int UNROLL, bool NC, bool DS>
 __global__ void __launch_bounds__(EW_BLOCK) ew_vec_kernel(EwArgs<T> p) {
   constexpr int VEC = 32 / sizeof(T);
   const int64_t tid = (int64_t)blockIdx.x * EW_BLOCK + threadIdx.x;
-  p.a = coef(p.a, p.an, p.ad);
-  p.b = coef(p.b, p.bn, p.bd);
+  if constexpr (DS) {
+    p.a = coef(p.a, p.an, p.ad);
+    p.b = coef(p.b, p.bn, p.bd);
+  }
 
   // Scalar head (to 32 B alignment) and tail (remainder of the body).
   const int64_t tail0 = p.head + p.nvec * VEC;
@@ -116,11 +121,13 @@ __global__ void __launch_bounds__(EW_BLOCK) ew_vec_kernel(EwArgs<T> p) {
 }
 
 // Arrays not co-aligned modulo 32 B: scalar grid-stride loop, still one pass.
-template <typename T, bool HAS_Y>
+template <typename T, bool HAS_Y, bool DS>
 __global__ void __launch_bounds__(EW_BLOCK) ew_scalar_kernel(EwArgs<T> p) {
   const int64_t nthreads = (int64_t)gridDim.x * EW_BLOCK;
-  p.a = coef(p.a, p.an, p.ad);
-  p.b = coef(p.b, p.bn, p.bd);
+  if constexpr (DS) {
+    p.a = coef(p.a, p.an, p.ad);
+    p.b = coef(p.b, p.bn, p.bd);
+  }
   for (int64_t i = (int64_t)blockIdx.x * EW_BLOCK + threadIdx.x; i < p.n; i += nthreads) {
     T y = HAS_Y ? p.y[i] : zero_of<T>();
     p.z[i] = stmt<T, HAS_Y>(p.a, p.x[i], p.b, y);
@@ -160,16 +167,18 @@ ga_status_t launch_ew(int64_t n, const ga_scalar_t &a, const void *x, const ga_s
   p.ad = static_cast<const T *>(ad);
   p.bn = static_cast<const T *>(bn);
   p.bd = static_cast<const T *>(bd);
+  const bool ds = an || ad || bn || bd;
 
   const uintptr_t phase = (uintptr_t)x & 31;
   const bool coaligned = ((uintptr_t)z & 31) == phase && (!HAS_Y || ((uintptr_t)y & 31) == phase) &&
                          (phase % sizeof(T)) == 0;
   if (!coaligned) {
-    const int max_grid = resident_grid((const void *)ew_scalar_kernel<T, HAS_Y>, EW_BLOCK);
+    const int max_grid = resident_grid((const void *)ew_scalar_kernel<T, HAS_Y, false>, EW_BLOCK);
     int grid = (int)std::min<int64_t>(cdiv(n, EW_BLOCK), max_grid);
     p.head = 0;
     p.nvec = 0;
-    ew_scalar_kernel<T, HAS_Y><<<grid, EW_BLOCK, 0, s>>>(p);
+    if (ds) ew_scalar_kernel<T, HAS_Y, true><<<grid, EW_BLOCK, 0, s>>>(p);
+    else ew_scalar_kernel<T, HAS_Y, false><<<grid, EW_BLOCK, 0, s>>>(p);
     count_launch();
     return check_launch("ew_scalar_kernel");
   }
@@ -179,8 +188,13 @@ ga_status_t launch_ew(int64_t n, const ga_scalar_t &a, const void *x, const ga_s
   // requires the data to stay unwritten for the kernel's lifetime.
   const bool inplace = z == x || (HAS_Y && z == y);
   int grid = (int)std::min<int64_t>(std::max<int64_t>(cdiv(p.nvec, CHUNK), 1), 0x7fffffffLL);
-  if (inplace) ew_vec_kernel<T, HAS_Y, UNROLL, false><<<grid, EW_BLOCK, 0, s>>>(p);
-  else ew_vec_kernel<T, HAS_Y, UNROLL, true><<<grid, EW_BLOCK, 0, s>>>(p);
+  if (ds) {
+    if (inplace) ew_vec_kernel<T, HAS_Y, UNROLL, false, true><<<grid, EW_BLOCK, 0, s>>>(p);
+    else ew_vec_kernel<T, HAS_Y, UNROLL, true, true><<<grid, EW_BLOCK, 0, s>>>(p);
+  } else {
+    if (inplace) ew_vec_kernel<T, HAS_Y, UNROLL, false, false><<<grid, EW_BLOCK, 0, s>>>(p);
+    else ew_vec_kernel<T, HAS_Y, UNROLL, true, false><<<grid, EW_BLOCK, 0, s>>>(p);
+  }
   count_launch();
   return check_launch("ew_vec_kernel");
 }
