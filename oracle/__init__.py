@@ -82,6 +82,11 @@ def lib():
         L.oracle_sum_complex.argtypes = [ctypes.c_int, ctypes.c_int, i64, vp, vp, vp, vp]
         L.oracle_norm2_complex.restype = d
         L.oracle_norm2_complex.argtypes = [ctypes.c_int, i64, vp]
+        for nm in ("oracle_ewmap_f32", "oracle_ewmap_f64"):
+            getattr(L, nm).restype = None
+            getattr(L, nm).argtypes = [ctypes.c_int, i64, vp, vp, vp]
+        L.oracle_ewmap_int.restype = None
+        L.oracle_ewmap_int.argtypes = [ctypes.c_int, ctypes.c_int, i64, vp, vp, vp]
         L.oracle_stencil3_f64.restype = None
         L.oracle_stencil3_f64.argtypes = [i64, d, d, d, vp, vp, vp]
         L.oracle_stencil3_f32.restype = None
@@ -240,3 +245,26 @@ def stencil3(l, d, u, x, diag=None):
     fn = lib().oracle_stencil3_f64 if x.dtype == np.float64 else lib().oracle_stencil3_f32
     fn(x.size, st(l).item(), st(d).item(), st(u).item(), _ptr(diag) if diag is not None else None, _ptr(x), _ptr(y))
     return y
+
+
+EW_MUL, EW_DIV, EW_SQRT, EW_ABS, EW_NEG, EW_EXP, EW_LOG, EW_SIN, EW_COS, EW_MAX, EW_MIN = range(11)
+EW_BINARY = (EW_MUL, EW_DIV, EW_MAX, EW_MIN)
+
+
+def ewmap(op, x, y=None):
+    """z = op(x[, y]) elementwise (PAPER.md:378-381; R26)."""
+    x = _c(x)
+    if op in EW_BINARY:
+        y = _c(y, x.dtype)
+        assert y.shape == x.shape
+    else:
+        y = None
+    z = np.empty_like(x)
+    L = lib()
+    if x.dtype == np.float32:
+        L.oracle_ewmap_f32(op, x.size, _ptr(x), _ptr(y), _ptr(z))
+    elif x.dtype == np.float64:
+        L.oracle_ewmap_f64(op, x.size, _ptr(x), _ptr(y), _ptr(z))
+    else:
+        L.oracle_ewmap_int(op, _DT[x.dtype], x.size, _ptr(x), _ptr(y), _ptr(z))
+    return z

@@ -475,3 +475,69 @@ void oracle_stencil3_f32(int64_t n, float l, float d, float u, const float *diag
     y[i] = acc;
   }
 }
+
+/* ------------------------------------------------------------------------ */
+/* GPUArray's other arithmetic operators and cumath-style unary maps        */
+/* (§8(f) NEXT-2: GPUArrays "support all arithmetic operators ... many      */
+/* special functions are available in pycuda.cumath").    */
+/* op: 0 MUL z=x*y, 1 DIV z=x/y, 2 SQRT, 3 ABS, 4 NEG, 5 EXP, 6 LOG,         */
+/*     7 SIN, 8 COS, 9 MAX (maxNum), 10 MIN (minNum).                         */
+/* IEEE-exact ops (MUL, DIV, SQRT, ABS, NEG, MAX, MIN) are one RN step; the  */
+/* transcendental ones are glibc's (R26 gives the ulp bound).       */
+/* Integers: MUL (wraps), ABS, NEG (wrap at INT_MIN), MAX, MIN.               */
+/* ------------------------------------------------------------------------ */
+void oracle_ewmap_f32(int op, int64_t n, const float *x, const float *y, float *z) {
+  for (int64_t i = 0; i < n; ++i) {
+    float a = x[i], b = y ? y[i] : 0.0f, r = 0.0f;
+    switch (op) {
+      case 0: r = a * b; break;
+      case 1: r = a / b; break;
+      case 2: r = sqrtf(a); break;
+      case 3: r = fabsf(a); break;
+      case 4: r = -a; break;
+      case 5: r = expf(a); break;
+      case 6: r = logf(a); break;
+      case 7: r = sinf(a); break;
+      case 8: r = cosf(a); break;
+      case 9: r = fmaxf(a, b); break;
+      case 10: r = fminf(a, b); break;
+    }
+    z[i] = r;
+  }
+}
+
+void oracle_ewmap_f64(int op, int64_t n, const double *x, const double *y, double *z) {
+  for (int64_t i = 0; i < n; ++i) {
+    double a = x[i], b = y ? y[i] : 0.0, r = 0.0;
+    switch (op) {
+      case 0: r = a * b; break;
+      case 1: r = a / b; break;
+      case 2: r = sqrt(a); break;
+      case 3: r = fabs(a); break;
+      case 4: r = -a; break;
+      case 5: r = exp(a); break;
+      case 6: r = log(a); break;
+      case 7: r = sin(a); break;
+      case 8: r = cos(a); break;
+      case 9: r = fmax(a, b); break;
+      case 10: r = fmin(a, b); break;
+    }
+    z[i] = r;
+  }
+}
+
+void oracle_ewmap_int(int op, int dt, int64_t n, const void *x, const void *y, void *z) {
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t a = load_int(dt, x, i), b = y ? (int64_t)load_int(dt, y, i) : 0, r = 0;
+    uint64_t ua = (uint64_t)a;
+    switch (op) {
+      case 0: r = (int64_t)(ua * (uint64_t)b); break;
+      case 3: r = a < 0 ? (int64_t)(0 - ua) : a; break;
+      case 4: r = (int64_t)(0 - ua); break;
+      case 9: r = a > b ? a : b; break;
+      case 10: r = a < b ? a : b; break;
+    }
+    if (dt == O_I32) ((int32_t *)z)[i] = (int32_t)(uint32_t)(uint64_t)r;
+    else ((int64_t *)z)[i] = r;
+  }
+}

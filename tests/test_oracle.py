@@ -506,3 +506,49 @@ def test_stencil3_poisson_closed_forms():
     r = np.arange(n, dtype=np.float64)
     y = oracle.stencil3(-1, 2, -1, r)
     assert np.all(y[1:-1] == 0) and y[0] == -1.0 and y[-1] == n
+
+
+# ------------------------------------------------------------ other operators / cumath maps (NEXT-2)
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_ewmap_float_against_numpy(dt):
+    """IEEE-exact ops equal numpy bit for bit; libm maps are within 1 ulp of
+    numpy's (both are faithful implementations)."""
+    x = synth.host_fill(synth.F32_S11 if dt == np.float32 else synth.F64_S11, 1, 4099) * dt(3)
+    y = synth.host_fill(synth.F32_S11 if dt == np.float32 else synth.F64_S11, 2, 4099) + dt(1.5)
+    ax = np.abs(x) + dt(1e-3)
+    with np.errstate(all="ignore"):
+        assert bits_equal(oracle.ewmap(oracle.EW_MUL, x, y), x * y)
+        assert bits_equal(oracle.ewmap(oracle.EW_DIV, x, y), x / y)
+        assert bits_equal(oracle.ewmap(oracle.EW_SQRT, ax), np.sqrt(ax))
+        assert bits_equal(oracle.ewmap(oracle.EW_ABS, x), np.abs(x))
+        assert bits_equal(oracle.ewmap(oracle.EW_NEG, x), -x)
+        assert bits_equal(oracle.ewmap(oracle.EW_MAX, x, y), np.fmax(x, y))
+        assert bits_equal(oracle.ewmap(oracle.EW_MIN, x, y), np.fmin(x, y))
+        for op, f, arg in ((oracle.EW_EXP, np.exp, x), (oracle.EW_LOG, np.log, ax), (oracle.EW_SIN, np.sin, x),
+                           (oracle.EW_COS, np.cos, x)):
+            got = oracle.ewmap(op, arg)
+            # reference: float64 evaluation rounded once (fp32 inputs: the
+            # correctly rounded value in all but rare cases); glibc is faithful
+            ref = f(arg.astype(np.float64)).astype(dt)
+            ulps = np.abs(got.view(np.int32 if dt == np.float32 else np.int64).astype(np.int64)
+                          - ref.view(np.int32 if dt == np.float32 else np.int64).astype(np.int64))
+            assert ulps.max() <= (1 if dt == np.float32 else 2), (op, ulps.max())
+    # special cases: sqrt(-1) = nan, log(0) = -inf, exp(0) = 1
+    with np.errstate(all="ignore"):
+        assert np.isnan(oracle.ewmap(oracle.EW_SQRT, np.array([-1.0], dt))[0])
+        assert oracle.ewmap(oracle.EW_LOG, np.array([0.0], dt))[0] == -np.inf
+        assert oracle.ewmap(oracle.EW_EXP, np.array([0.0], dt))[0] == 1.0
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.int64])
+def test_ewmap_int_wraps(dt):
+    info = np.iinfo(dt)
+    x = RNG.integers(info.min, info.max, size=3001, dtype=dt, endpoint=True)
+    y = RNG.integers(info.min, info.max, size=3001, dtype=dt, endpoint=True)
+    x[0] = info.min
+    with np.errstate(over="ignore"):
+        assert bits_equal(oracle.ewmap(oracle.EW_MUL, x, y), x * y)
+        assert bits_equal(oracle.ewmap(oracle.EW_NEG, x), -x)
+        assert bits_equal(oracle.ewmap(oracle.EW_ABS, x), np.abs(x))   # abs(INT_MIN) wraps to INT_MIN
+    assert bits_equal(oracle.ewmap(oracle.EW_MAX, x, y), np.maximum(x, y))
+    assert bits_equal(oracle.ewmap(oracle.EW_MIN, x, y), np.minimum(x, y))
