@@ -118,6 +118,22 @@ ga_status_t gpuarray_axpbyz_ds(ga_dtype_t dt, int64_t n, ga_dscalar_t a, const v
 ga_status_t gpuarray_axpbz(ga_dtype_t dt, int64_t n, ga_scalar_t a, const void *x, ga_scalar_t b,
                            void *z, void *stream);
 
+/* ---- The other GPUArray operators and cumath-style maps (SURVEY.md §8(f)
+ * NEXT-2; "support all arithmetic operators ... many special functions are
+ * available in pycuda.cumath").  Binary: z = x*y, x/y,
+ * maxNum(x,y), minNum(x,y); unary (y ignored, may be NULL): sqrt, |x|, -x,
+ * exp, log, sin, cos.  F32/F64: MUL, DIV, SQRT, ABS, NEG, MAX, MIN are IEEE
+ * round-to-nearest (bit-exact against the oracle); EXP, LOG, SIN, COS are
+ * CUDA's accurate device functions (R26: within a few ulp of
+ * glibc).  I32/I64: MUL (wrapping), ABS, NEG (wrapping at INT_MIN), MAX, MIN;
+ * others GA_ERR_UNSUPPORTED.  z may equal x or y; n == 0: no-op. */
+typedef enum {
+  GA_EW_MUL = 0, GA_EW_DIV = 1, GA_EW_SQRT = 2, GA_EW_ABS = 3, GA_EW_NEG = 4, GA_EW_EXP = 5,
+  GA_EW_LOG = 6, GA_EW_SIN = 7, GA_EW_COS = 8, GA_EW_MAX = 9, GA_EW_MIN = 10
+} ga_ewop_t;
+ga_status_t gpuarray_elementwise(ga_ewop_t op, ga_dtype_t dt, int64_t n, const void *x, const void *y, void *z,
+                                 void *stream);
+
 /* Bytes of workspace gpuarray_reduce needs (an upper bound for every n and
  * every device).  The workspace must be zero-filled ONCE when allocated; the
  * kernel leaves it reusable (the completion ticket resets itself).  Calls

@@ -22,7 +22,7 @@ EXPORTS = (
     "gpuarray_axpbyz", "gpuarray_axpbz", "gpuarray_reduce_workspace_bytes", "gpuarray_reduce",
     "gpuarray_scan_workspace_bytes", "gpuarray_scan", "gpuarray_status_string", "gpuarray_last_error",
     "gpuarray_abi_version", "gpuarray_launch_count", "gpuarray_xgpu_buffer_bytes", "gpuarray_reduce_xgpu",
-    "gpuarray_stencil3", "gpuarray_axpbyz_ds",
+    "gpuarray_stencil3", "gpuarray_axpbyz_ds", "gpuarray_elementwise",
 )
 
 
@@ -113,6 +113,8 @@ def _load():
     lib.gpuarray_reduce_xgpu.restype = st
     lib.gpuarray_reduce_xgpu.argtypes = [st, st, st, st, i64, vp, vp, vp, vp, sz, vp, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_uint64, st, vp]
+    lib.gpuarray_elementwise.restype = st
+    lib.gpuarray_elementwise.argtypes = [st, st, i64, vp, vp, vp, vp]
     lib.gpuarray_axpbyz_ds.restype = st
     lib.gpuarray_axpbyz_ds.argtypes = [st, i64, ga_dscalar_t, vp, ga_dscalar_t, vp, vp, vp]
     lib.gpuarray_stencil3.restype = st
@@ -162,6 +164,14 @@ def gpuarray_scan_workspace_bytes(dt, n):
 
 def gpuarray_scan(op, kind, dt, n, in_, out, carry, carry_count, workspace, workspace_bytes, stream):
     return LIB.gpuarray_scan(op, kind, dt, n, in_, out, carry, carry_count, workspace, workspace_bytes, stream)
+
+
+GA_EW_MUL, GA_EW_DIV, GA_EW_SQRT, GA_EW_ABS, GA_EW_NEG, GA_EW_EXP, GA_EW_LOG, GA_EW_SIN, GA_EW_COS, GA_EW_MAX, \
+    GA_EW_MIN = range(11)
+
+
+def gpuarray_elementwise(op, dt, n, x, y, z, stream):
+    return LIB.gpuarray_elementwise(op, dt, n, x, y, z, stream)
 
 
 def gpuarray_axpbyz_ds(dt, n, a, x, b, y, z, stream):

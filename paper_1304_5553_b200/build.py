@@ -41,12 +41,25 @@ def stale():
 
 
 def build(force=False, verbose=False):
+    """Compile every csrc/*.cu to an object in parallel, then link."""
     if not force and not stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *SOURCES]
-    if verbose:
-        print(" ".join(cmd), flush=True)
-    subprocess.check_call(cmd)
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared",)]
+    jobs = []
+    for src in SOURCES:
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        jobs.append((obj, [nvcc(), *compile_flags, "-I", os.path.join(ROOT, "include"), "-c", "-o", obj, src]))
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
+        for obj, cmd in jobs:
+            if verbose:
+                print(" ".join(cmd), flush=True)
+        list(ex.map(lambda j: subprocess.check_call(j[1]), jobs))
+    link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+            "-o", LIB + ".tmp", *[o for o, _ in jobs]]
+    subprocess.check_call(link)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -65,6 +65,10 @@ ga_status_t launch_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_t 
 ga_status_t launch_stencil3(ga_dtype_t dt, int64_t n, const ga_scalar_t &l, const ga_scalar_t &d,
                             const ga_scalar_t &u, const void *diag, const void *x, void *y, cudaStream_t s);
 
+bool ewop_binary(ga_ewop_t op);
+ga_status_t launch_ewmap(ga_ewop_t op, ga_dtype_t dt, int64_t n, const void *x, const void *y, void *z,
+                         cudaStream_t s);
+
 size_t reduce_workspace_bytes();
 size_t scan_workspace_bytes(ga_dtype_t dt, int64_t n);
 

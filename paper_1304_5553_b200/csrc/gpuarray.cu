@@ -187,6 +187,20 @@ ga_status_t gpuarray_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_
   return launch_scan(op, kind, dt, n, in, out, carry, carry_count, workspace, (cudaStream_t)stream);
 }
 
+ga_status_t gpuarray_elementwise(ga_ewop_t op, ga_dtype_t dt, int64_t n, const void *x, const void *y, void *z,
+                                 void *stream) {
+  if (op < GA_EW_MUL || op > GA_EW_MIN) return fail(GA_ERR_INVALID_ARGUMENT, "elementwise: bad op %d", (int)op);
+  if (!valid_dtype(dt)) return fail(GA_ERR_INVALID_ARGUMENT, "elementwise: bad dtype %d", (int)dt);
+  if (n < 0) return fail(GA_ERR_INVALID_ARGUMENT, "elementwise: n < 0");
+  if (n == 0) return GA_OK;
+  const bool bin = ewop_binary(op);
+  if (!x || !z || (bin && !y)) return fail(GA_ERR_INVALID_ARGUMENT, "elementwise: NULL array with n > 0");
+  const size_t bytes = (size_t)n * dtype_size(dt);
+  if (partial_overlap(z, bytes, x, bytes) || (bin && partial_overlap(z, bytes, y, bytes)))
+    return fail(GA_ERR_INVALID_ARGUMENT, "elementwise: z partially overlaps an input");
+  return launch_ewmap(op, dt, n, x, bin ? y : nullptr, z, (cudaStream_t)stream);
+}
+
 ga_status_t gpuarray_stencil3(ga_dtype_t dt, int64_t n, ga_scalar_t l, ga_scalar_t d, ga_scalar_t u,
                               const void *diag, const void *x, void *y, void *stream) {
   if (!valid_dtype(dt)) return fail(GA_ERR_INVALID_ARGUMENT, "stencil3: bad dtype %d", (int)dt);

@@ -159,6 +159,70 @@ def stencil3(l, d, u, x, diag=None, out=None):
     return out
 
 
+# --------------------------------------------------------------- operators / cumath
+_BINARY = (_abi.GA_EW_MUL, _abi.GA_EW_DIV, _abi.GA_EW_MAX, _abi.GA_EW_MIN)
+
+
+def elementwise(op, x, y=None, out=None):
+    """z = op(x[, y]) in one pass (gpuarray_elementwise; PAPER.md:378-381)."""
+    _check_array("x", x)
+    if op in _BINARY:
+        if y is None:
+            raise ValueError("binary operator needs y")
+        _same(x, y, "y")
+    if out is None:
+        out = torch.empty_like(x)
+    else:
+        _same(x, out, "out")
+    check(_abi.gpuarray_elementwise(op, ga_dtype(x.dtype), x.numel(), _ptr(x), _ptr(y) if op in _BINARY else None,
+                                    _ptr(out), _stream(x)))
+    return out
+
+
+def multiply(x, y, out=None):
+    return elementwise(_abi.GA_EW_MUL, x, y, out)
+
+
+def divide(x, y, out=None):
+    return elementwise(_abi.GA_EW_DIV, x, y, out)
+
+
+def maximum(x, y, out=None):
+    return elementwise(_abi.GA_EW_MAX, x, y, out)
+
+
+def minimum(x, y, out=None):
+    return elementwise(_abi.GA_EW_MIN, x, y, out)
+
+
+def sqrt(x, out=None):
+    return elementwise(_abi.GA_EW_SQRT, x, None, out)
+
+
+def fabs(x, out=None):
+    return elementwise(_abi.GA_EW_ABS, x, None, out)
+
+
+def negative(x, out=None):
+    return elementwise(_abi.GA_EW_NEG, x, None, out)
+
+
+def exp(x, out=None):
+    return elementwise(_abi.GA_EW_EXP, x, None, out)
+
+
+def log(x, out=None):
+    return elementwise(_abi.GA_EW_LOG, x, None, out)
+
+
+def sin(x, out=None):
+    return elementwise(_abi.GA_EW_SIN, x, None, out)
+
+
+def cos(x, out=None):
+    return elementwise(_abi.GA_EW_COS, x, None, out)
+
+
 # --------------------------------------------------------------- map-reduce
 def reduce(op, map_, x, y=None, out_dtype=None, out=None):
     """Fold map(x, y) with op from its neutral element; returns a 0-d device

@@ -471,3 +471,63 @@ def test_complex_closed_forms_and_errors():
         G.max(ones)
     with pytest.raises(TypeError):
         G.scan(ones)
+
+
+# ------------------------------------------------------------------ operators / cumath maps (NEXT-2)
+EW_EXACT = [oracle.EW_MUL, oracle.EW_DIV, oracle.EW_SQRT, oracle.EW_ABS, oracle.EW_NEG, oracle.EW_MAX, oracle.EW_MIN]
+EW_LIBM = [oracle.EW_EXP, oracle.EW_LOG, oracle.EW_SIN, oracle.EW_COS]
+
+
+def ulp_dist(a, b):
+    it = np.int32 if a.dtype == np.float32 else np.int64
+    ka, kb = a.view(it).astype(np.int64), b.view(it).astype(np.int64)
+    ka = np.where(ka < 0, np.iinfo(it).min - ka, ka)  # monotone key for sign-magnitude floats
+    kb = np.where(kb < 0, np.iinfo(it).min - kb, kb)
+    d = np.abs(ka - kb)
+    both_nan = np.isnan(a) & np.isnan(b)
+    return np.where(both_nan, 0, d)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("n", [1, 33, 4097, 1_000_003])
+def test_ewmap_float(dt, n):
+    x = host_data(dt, n, 1, signed=True) * dt(8)
+    y = host_data(dt, n, 2, signed=True) + dt(1.5)
+    ax = np.abs(x) + dt(1e-3)
+    for op in EW_EXACT + EW_LIBM:
+        arg = ax if op in (oracle.EW_SQRT, oracle.EW_LOG) else x
+        with np.errstate(all="ignore"):
+            ref = oracle.ewmap(op, arg, y)
+        for offs in (0, 1):
+            got = G.elementwise(op, to_dev(arg, offs), to_dev(y, offs) if op in G._BINARY else None).cpu().numpy()
+            if op in EW_EXACT:
+                assert_bit_exact(got, ref)
+            else:  # R26: CUDA accurate functions vs glibc
+                assert ulp_dist(got, ref).max() <= 3, (op, int(ulp_dist(got, ref).max()))
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.int64])
+def test_ewmap_int(dt):
+    info = np.iinfo(dt)
+    rng = np.random.default_rng(9)
+    x = rng.integers(info.min, info.max, size=100_003, dtype=dt, endpoint=True)
+    y = rng.integers(info.min, info.max, size=100_003, dtype=dt, endpoint=True)
+    x[5] = info.min
+    for op in (oracle.EW_MUL, oracle.EW_ABS, oracle.EW_NEG, oracle.EW_MAX, oracle.EW_MIN):
+        got = G.elementwise(op, to_dev(x), to_dev(y) if op in G._BINARY else None).cpu().numpy()
+        assert_bit_exact(got, oracle.ewmap(op, x, y))
+    with pytest.raises(TypeError):
+        G.divide(to_dev(x), to_dev(y))   # integer division is not instantiated
+
+
+def test_ewmap_special_values_and_inplace():
+    x = np.array([0.0, -0.0, 1.0, -1.0, np.inf, -np.inf, np.nan, 1e-40, 4.0], np.float32)
+    with np.errstate(all="ignore"):
+        for op in (oracle.EW_SQRT, oracle.EW_LOG, oracle.EW_EXP, oracle.EW_ABS, oracle.EW_NEG):
+            got = G.elementwise(op, to_dev(x)).cpu().numpy()
+            ref = oracle.ewmap(op, x)
+            assert ulp_dist(got, ref).max() <= (0 if op in EW_EXACT else 3), op
+    xd = to_dev(x[np.isfinite(x)])
+    G.sqrt(G.fabs(xd, out=xd), out=xd)
+    with np.errstate(all="ignore"):
+        assert_bit_exact(xd.cpu().numpy(), np.sqrt(np.abs(x[np.isfinite(x)])))
