@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define GPUARRAY_ABI_VERSION 2
+#define GPUARRAY_ABI_VERSION 3
 
 /* C64 / C128: complex numbers as interleaved (re, im) float / double pairs
  * ("seamless support for complex numbers"; §8(f) NEXT-3). */
@@ -189,26 +189,32 @@ ga_status_t gpuarray_reduce_xgpu(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_
                                  const uint64_t *peer_buffers, int rank, int world, uint64_t seq,
                                  ga_xgpu_fold_t fold, void *stream);
 
-/* Bytes of workspace gpuarray_scan needs for (dt, n): a 256-byte header plus
- * per-tile look-back status.  Zero-fill once; reusable afterwards (status
- * words are epoch-tagged, the tile counter resets itself).  Never share it
- * with gpuarray_reduce.  A corrupted workspace makes the kernel trap (a CUDA
- * error at the next synchronisation) after 10 s instead of hanging. */
+/* Bytes of workspace gpuarray_scan needs for (dt, n), dt = the scan's OUTPUT
+ * dtype: a 256-byte header plus per-tile look-back status.  Zero-fill once;
+ * reusable afterwards (status words are epoch-tagged, the tile counter resets
+ * itself).  Never share it with gpuarray_reduce.  A corrupted workspace makes
+ * the kernel trap (a CUDA error at the next synchronisation) after 10 s
+ * instead of hanging. */
 size_t gpuarray_scan_workspace_bytes(ga_dtype_t dt, int64_t n);
 
-/* Scan with the reduction expression op ∈ {SUM, MAX, MIN} (written ⊕ below),
- * dt in {F32, F64, I32, I64} (complex: GA_ERR_UNSUPPORTED):
- *   inclusive: out[i] = c ⊕ in[0] ⊕ ... ⊕ in[i]
- *   exclusive: out[0] = c, out[i] = c ⊕ in[0] ⊕ ... ⊕ in[i-1]   (R13)
- * where c = carry[0] ⊕ ... ⊕ carry[carry_count-1] (a device array of dt; c is
- * the neutral element when carry_count == 0).  The carry is how a sharded
- * scan passes the totals of earlier shards.  Integers
- * wrap (R4, R14); MAX/MIN are exact (maxNum/minNum for floats, R6); float
- * SUM is a tree/look-back-ordered approximation of the exact prefix sums
- * (R22), not bit-reproducible run to run.  out may equal in
- * (in-place); other overlap is invalid.  n == 0: no-op. */
-ga_status_t gpuarray_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_t n, const void *in,
-                          void *out, const void *carry, int64_t carry_count, void *workspace,
+/* Scan (§3.2.6 "parallel prefix sums") with the reduction
+ * expression op ∈ {SUM, MAX, MIN} (written ⊕ below):
+ *   inclusive: out[i] = c ⊕ w(in[0]) ⊕ ... ⊕ w(in[i])
+ *   exclusive: out[0] = c, out[i] = c ⊕ w(in[0]) ⊕ ... ⊕ w(in[i-1])   (R13)
+ * in_dt == out_dt ∈ {F32, F64, I32, I64}, or the widening scans in_dt = I32,
+ * out_dt = I64 and in_dt = F32, out_dt = F64 (NEXT-2; the paper makes the
+ * result dtype a parameter); w() is the exact conversion to out_dt
+ * and the scan runs in out_dt.  Other pairs and complex: GA_ERR_UNSUPPORTED.
+ * c = carry[0] ⊕ ... ⊕ carry[carry_count-1] is a device array of out_dt (the
+ * neutral element when carry_count == 0); it is how a sharded scan passes
+ * the totals of earlier shards.  Integers wrap (R4,
+ * R14); MAX/MIN are exact (maxNum/minNum for floats, R6); float SUM is a
+ * tree/look-back-ordered approximation of the exact prefix sums (DESIGN.md
+ * R22), not bit-reproducible run to run.  in: n elements of in_dt; out: n
+ * elements of out_dt.  out may equal in when in_dt == out_dt (in-place);
+ * any other overlap is GA_ERR_INVALID_ARGUMENT.  n == 0: no-op. */
+ga_status_t gpuarray_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
+                          const void *in, void *out, const void *carry, int64_t carry_count, void *workspace,
                           size_t workspace_bytes, void *stream);
 
 /* ---- Operator of the CG workload (the paper's

@@ -205,13 +205,21 @@ NEUTRAL = {
 }
 
 
-def scan(kind, x, carry=None, out=None, op=SUM, return_sumabs=False):
+def scan(kind, x, carry=None, out=None, op=SUM, return_sumabs=False, out_dtype=None):
     """Scan with reduction expression `op`; the exclusive
     head / inclusive start is `carry` (default: the neutral element, R13).
     Integer SUM wraps in the element type; float SUM returns the exact prefix
     sums as float64 (and, with return_sumabs, |c| + sum |x_j| per position);
-    MAX / MIN fold with maxNum/minNum and return the element type."""
+    MAX / MIN fold with maxNum/minNum and return the element type.
+    out_dtype widens first (int32 -> int64, float32 -> float64: the result
+    dtype is a parameter): the scan of the exactly converted
+    elements, i.e. the scan run in the wide type (R27)."""
     x = _c(x)
+    if out_dtype is not None and np.dtype(out_dtype) != x.dtype:
+        if (x.dtype, np.dtype(out_dtype)) not in ((np.dtype(np.int32), np.dtype(np.int64)),
+                                                  (np.dtype(np.float32), np.dtype(np.float64))):
+            raise TypeError(f"no widening scan {x.dtype} -> {np.dtype(out_dtype)}")
+        x = x.astype(out_dtype)  # exact conversion
     L = lib()
     if op == SUM and x.dtype.kind == "f":
         res = np.empty(x.size, np.float64)

@@ -99,7 +99,7 @@ def _load():
     lib.gpuarray_scan_workspace_bytes.restype = sz
     lib.gpuarray_scan_workspace_bytes.argtypes = [st, i64]
     lib.gpuarray_scan.restype = st
-    lib.gpuarray_scan.argtypes = [st, st, st, i64, vp, vp, vp, i64, vp, sz, vp]
+    lib.gpuarray_scan.argtypes = [st, st, st, st, i64, vp, vp, vp, i64, vp, sz, vp]
     lib.gpuarray_status_string.restype = ctypes.c_char_p
     lib.gpuarray_status_string.argtypes = [st]
     lib.gpuarray_last_error.restype = ctypes.c_char_p
@@ -162,8 +162,9 @@ def gpuarray_scan_workspace_bytes(dt, n):
     return LIB.gpuarray_scan_workspace_bytes(dt, n)
 
 
-def gpuarray_scan(op, kind, dt, n, in_, out, carry, carry_count, workspace, workspace_bytes, stream):
-    return LIB.gpuarray_scan(op, kind, dt, n, in_, out, carry, carry_count, workspace, workspace_bytes, stream)
+def gpuarray_scan(op, kind, in_dt, out_dt, n, in_, out, carry, carry_count, workspace, workspace_bytes, stream):
+    return LIB.gpuarray_scan(op, kind, in_dt, out_dt, n, in_, out, carry, carry_count, workspace, workspace_bytes,
+                             stream)
 
 
 GA_EW_MUL, GA_EW_DIV, GA_EW_SQRT, GA_EW_ABS, GA_EW_NEG, GA_EW_EXP, GA_EW_LOG, GA_EW_SIN, GA_EW_COS, GA_EW_MAX, \

@@ -59,7 +59,8 @@ ga_status_t launch_axpbz(ga_dtype_t dt, int64_t n, const ga_scalar_t &a, const v
                          const ga_scalar_t &b, void *z, cudaStream_t s);
 ga_status_t launch_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
                           const void *x, const void *y, void *out, void *ws, const Exchange &xg, cudaStream_t s);
-ga_status_t launch_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_t n, const void *in, void *out,
+ga_status_t launch_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t in_dt, ga_dtype_t dt, int64_t n, const void *in,
+                        void *out,
                         const void *carry, int64_t carry_count, void *ws, cudaStream_t s);
 
 ga_status_t launch_stencil3(ga_dtype_t dt, int64_t n, const ga_scalar_t &l, const ga_scalar_t &d,

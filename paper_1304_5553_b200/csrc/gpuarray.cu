@@ -167,24 +167,31 @@ ga_status_t gpuarray_reduce_xgpu(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_
 
 size_t gpuarray_scan_workspace_bytes(ga_dtype_t dt, int64_t n) { return n < 0 ? 0 : scan_workspace_bytes(dt, n); }
 
-ga_status_t gpuarray_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_t n, const void *in, void *out,
-                          const void *carry, int64_t carry_count, void *workspace, size_t workspace_bytes,
-                          void *stream) {
+ga_status_t gpuarray_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
+                          const void *in, void *out, const void *carry, int64_t carry_count, void *workspace,
+                          size_t workspace_bytes, void *stream) {
   if (op < GA_OP_SUM || op > GA_OP_MIN) return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad op %d", (int)op);
   if (kind != GA_SCAN_INCLUSIVE && kind != GA_SCAN_EXCLUSIVE)
     return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad kind %d", (int)kind);
-  if (!valid_dtype(dt)) return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad dtype %d", (int)dt);
-  if (dt == GA_C64 || dt == GA_C128) return fail(GA_ERR_UNSUPPORTED, "scan: complex not instantiated");
+  if (!valid_dtype(in_dt) || !valid_dtype(out_dt))
+    return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad dtype %d -> %d", (int)in_dt, (int)out_dt);
+  if (in_dt == GA_C64 || in_dt == GA_C128 || out_dt == GA_C64 || out_dt == GA_C128)
+    return fail(GA_ERR_UNSUPPORTED, "scan: complex not instantiated");
+  if (in_dt != out_dt && !((in_dt == GA_I32 && out_dt == GA_I64) || (in_dt == GA_F32 && out_dt == GA_F64)))
+    return fail(GA_ERR_UNSUPPORTED, "scan %d -> %d not instantiated (widening: int32 -> int64, float32 -> float64)",
+                (int)in_dt, (int)out_dt);
   if (n < 0) return fail(GA_ERR_INVALID_ARGUMENT, "scan: n < 0");
   if (carry_count < 0 || (carry_count > 0 && !carry))
     return fail(GA_ERR_INVALID_ARGUMENT, "scan: carry_count < 0 or carry NULL");
   if (n == 0) return GA_OK;
   if (!in || !out) return fail(GA_ERR_INVALID_ARGUMENT, "scan: NULL array with n > 0");
-  const size_t bytes = (size_t)n * dtype_size(dt);
-  if (partial_overlap(out, bytes, in, bytes)) return fail(GA_ERR_INVALID_ARGUMENT, "scan: out partially overlaps in");
-  const size_t need = scan_workspace_bytes(dt, n);
+  const size_t in_bytes = (size_t)n * dtype_size(in_dt), out_bytes = (size_t)n * dtype_size(out_dt);
+  if (in_dt == out_dt ? partial_overlap(out, out_bytes, in, in_bytes)
+                      : (in == out || partial_overlap(out, out_bytes, in, in_bytes)))
+    return fail(GA_ERR_INVALID_ARGUMENT, "scan: out overlaps in (a widening scan cannot run in place)");
+  const size_t need = scan_workspace_bytes(out_dt, n);
   if (!workspace || workspace_bytes < need) return fail(GA_ERR_WORKSPACE, "scan: workspace needs %zu bytes", need);
-  return launch_scan(op, kind, dt, n, in, out, carry, carry_count, workspace, (cudaStream_t)stream);
+  return launch_scan(op, kind, in_dt, out_dt, n, in, out, carry, carry_count, workspace, (cudaStream_t)stream);
 }
 
 ga_status_t gpuarray_elementwise(ga_ewop_t op, ga_dtype_t dt, int64_t n, const void *x, const void *y, void *z,

@@ -57,42 +57,47 @@ size_t ws_bytes(int64_t n) {
   return HEADER + status_bytes<T>(cdiv(n, min_tile));
 }
 
-template <int OP, typename T, bool EXCLUSIVE>
+// Tin != T: the widened scans (int32 -> int64, float -> double; NEXT-2),
+// same kernels, the input converted on load; a widened row stores 32 bytes
+// per lane, so the super-tile path needs a 32-byte aligned output.
+template <int OP, typename T, typename Tin, bool EXCLUSIVE>
 ga_status_t run(int64_t n, const void *in, void *out, const void *carry, int64_t carry_count, void *ws,
                 cudaStream_t s) {
-  const bool aligned = ((uintptr_t)in & 15) == 0 && ((uintptr_t)out & 15) == 0;
+  constexpr uintptr_t OUT_ALIGN = sizeof(T) == sizeof(Tin) ? 16 : 32;
+  const bool aligned = ((uintptr_t)in & 15) == 0 && ((uintptr_t)out & (OUT_ALIGN - 1)) == 0;
   const bool inplace = in == out;
   if (aligned) {
-    ScanArgs<T> p = make_args<T>(n, l2_tile<T>(), in, out, carry, carry_count, ws);
+    ScanArgs<T, Tin> p = make_args<T, Tin>(n, l2_tile<Tin>(), in, out, carry, carry_count, ws);
     const int grid = (int)p.num_tiles;
     if (inplace)
-      scan_l2_kernel<OP, T, L2_WARPS, L2_ROWS, L2_UNROLL, L2_DEPTH, false, EXCLUSIVE, true>
+      scan_l2_kernel<OP, T, Tin, L2_WARPS, L2_ROWS, L2_UNROLL, L2_DEPTH, false, EXCLUSIVE, true>
           <<<grid, L2_WARPS * 32, 0, s>>>(p);
     else
-      scan_l2_kernel<OP, T, L2_WARPS, L2_ROWS, L2_UNROLL, L2_DEPTH, true, EXCLUSIVE, true>
+      scan_l2_kernel<OP, T, Tin, L2_WARPS, L2_ROWS, L2_UNROLL, L2_DEPTH, true, EXCLUSIVE, true>
           <<<grid, L2_WARPS * 32, 0, s>>>(p);
   } else {
-    ScanArgs<T> p = make_args<T>(n, (int64_t)RG_BLOCK * RG_ITEMS, in, out, carry, carry_count, ws);
+    ScanArgs<T, Tin> p = make_args<T, Tin>(n, (int64_t)RG_BLOCK * RG_ITEMS, in, out, carry, carry_count, ws);
     if (p.num_tiles > 0x7fffffffLL) return fail(GA_ERR_UNSUPPORTED, "scan: n too large (%lld)", (long long)n);
-    scan_reg_kernel<OP, T, RG_BLOCK, RG_ITEMS, RG_DEPTH, EXCLUSIVE><<<(int)p.num_tiles, RG_BLOCK, 0, s>>>(p);
+    scan_reg_kernel<OP, T, Tin, RG_BLOCK, RG_ITEMS, RG_DEPTH, EXCLUSIVE><<<(int)p.num_tiles, RG_BLOCK, 0, s>>>(p);
   }
   count_launch();
   return check_launch("scan_kernel");
 }
 
-template <int OP, typename T>
+template <int OP, typename T, typename Tin>
 ga_status_t by_kind(bool ex, int64_t n, const void *in, void *out, const void *carry, int64_t cc, void *ws,
                     cudaStream_t s) {
-  return ex ? run<OP, T, true>(n, in, out, carry, cc, ws, s) : run<OP, T, false>(n, in, out, carry, cc, ws, s);
+  return ex ? run<OP, T, Tin, true>(n, in, out, carry, cc, ws, s)
+            : run<OP, T, Tin, false>(n, in, out, carry, cc, ws, s);
 }
 
-template <typename T>
+template <typename T, typename Tin = T>
 ga_status_t by_op(ga_op_t op, bool ex, int64_t n, const void *in, void *out, const void *carry, int64_t cc, void *ws,
                   cudaStream_t s) {
   switch (op) {
-    case GA_OP_SUM: return by_kind<GA_OP_SUM, T>(ex, n, in, out, carry, cc, ws, s);
-    case GA_OP_MAX: return by_kind<GA_OP_MAX, T>(ex, n, in, out, carry, cc, ws, s);
-    case GA_OP_MIN: return by_kind<GA_OP_MIN, T>(ex, n, in, out, carry, cc, ws, s);
+    case GA_OP_SUM: return by_kind<GA_OP_SUM, T, Tin>(ex, n, in, out, carry, cc, ws, s);
+    case GA_OP_MAX: return by_kind<GA_OP_MAX, T, Tin>(ex, n, in, out, carry, cc, ws, s);
+    case GA_OP_MIN: return by_kind<GA_OP_MIN, T, Tin>(ex, n, in, out, carry, cc, ws, s);
   }
   return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad op %d", (int)op);
 }
@@ -109,9 +114,14 @@ size_t scan_workspace_bytes(ga_dtype_t dt, int64_t n) {
   }
 }
 
-ga_status_t launch_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t dt, int64_t n, const void *in, void *out,
-                        const void *carry, int64_t carry_count, void *ws, cudaStream_t s) {
+ga_status_t launch_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t in_dt, ga_dtype_t dt, int64_t n, const void *in,
+                        void *out, const void *carry, int64_t carry_count, void *ws, cudaStream_t s) {
   const bool ex = kind == GA_SCAN_EXCLUSIVE;
+  if (in_dt != dt) {
+    if (in_dt == GA_I32 && dt == GA_I64) return by_op<int64_t, int32_t>(op, ex, n, in, out, carry, carry_count, ws, s);
+    if (in_dt == GA_F32 && dt == GA_F64) return by_op<double, float>(op, ex, n, in, out, carry, carry_count, ws, s);
+    return fail(GA_ERR_UNSUPPORTED, "scan %d -> %d not instantiated", (int)in_dt, (int)dt);
+  }
   switch (dt) {
     case GA_I32: return by_op<int32_t>(op, ex, n, in, out, carry, carry_count, ws, s);
     case GA_I64: return by_op<int64_t>(op, ex, n, in, out, carry, carry_count, ws, s);

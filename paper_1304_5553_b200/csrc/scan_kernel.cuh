@@ -100,11 +100,13 @@ struct Status<T, 8> {
   }
 };
 
-template <typename T>
+// Tin: the input element type; T: the scan (accumulator, output, status,
+// carry) type — equal, or a widening int32 -> int64 / float -> double.
+template <typename T, typename Tin = T>
 struct ScanArgs {
   int64_t n;
   int64_t num_tiles;
-  const T *in;
+  const Tin *in;
   T *out;
   const T *carry;
   int64_t carry_count;
@@ -180,8 +182,8 @@ __device__ T look_back(const Status<T> &st, int64_t tile, uint32_t epoch) {
 }
 
 // Carry-in: fold of carry[0..carry_count) in index order (neutral if none).
-template <int OP, typename T>
-__device__ __forceinline__ T carry_in(const ScanArgs<T> &p) {
+template <int OP, typename T, typename Tin>
+__device__ __forceinline__ T carry_in(const ScanArgs<T, Tin> &p) {
   T c = Op<OP, T>::neutral();
   for (int64_t k = 0; k < p.carry_count; ++k) c = Op<OP, T>::fold(c, p.carry[k]);
   return c;
@@ -285,6 +287,12 @@ __device__ __forceinline__ uint4 ldg128_hint(const void *p, uint64_t pol) {
                  : "memory");
   return v;
 }
+// 32 bytes per lane (a widened row: 4 int64 / double outputs per lane).
+__device__ __forceinline__ void stg256_hint(void *p, const uint4 &a, const uint4 &b, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(p),
+               "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void stg128_hint(void *p, const uint4 &v, uint64_t pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
@@ -294,8 +302,8 @@ __device__ __forceinline__ void stg128_hint(void *p, const uint4 &v, uint64_t po
 
 // Draw {epoch, tile id}; the CTA drawing the last id resets the counter and
 // bumps the epoch (every CTA has drawn by then).
-template <typename T>
-__device__ __forceinline__ void draw_tile(const ScanArgs<T> &p, uint32_t &tile, uint32_t &epoch) {
+template <typename A>
+__device__ __forceinline__ void draw_tile(const A &p, uint32_t &tile, uint32_t &epoch) {
   const unsigned long long old = atomicAdd(p.ticket, 1ull);
   tile = (uint32_t)old;
   epoch = (uint32_t)(old >> 32) & EPOCH_MASK;
@@ -314,11 +322,14 @@ __device__ __forceinline__ void draw_tile(const ScanArgs<T> &p, uint32_t &tile, 
 //   phase 3  every warp re-reads its slice (now L2-resident, evict_first),
 //            scans it row by row and stores (STG.128, 512 B per warp).
 // ===========================================================================
-template <int OP, typename T, int WARPS, int ROWS, int UNROLL, int DEPTH, bool NC, bool EXCLUSIVE, bool EARLY>
-__global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T> p) {
+template <int OP, typename T, typename Tin, int WARPS, int ROWS, int UNROLL, int DEPTH, bool NC, bool EXCLUSIVE,
+          bool EARLY>
+__global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p) {
   using O = Op<OP, T>;
-  constexpr int E = Chunk<T>::E;
-  constexpr int ROW = 32 * E;  // elements per 512-byte row
+  constexpr int E = Chunk<Tin>::E;  // elements per lane per row
+  constexpr int ROW = 32 * E;       // elements per row: 512 bytes of input
+  constexpr bool WIDEN = sizeof(T) != sizeof(Tin);
+  static_assert(!WIDEN || (sizeof(T) == 8 && sizeof(Tin) == 4), "widening is 4 -> 8 bytes");
   constexpr int64_t TILE = (int64_t)WARPS * ROWS * ROW;
   static_assert(ROWS % UNROLL == 0, "ROWS must be a multiple of UNROLL");
   static_assert(WARPS <= 32, "slice folds are scanned by one warp");
@@ -344,10 +355,13 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T> p) {
   auto load_row = [&](int r, uint64_t pol, T (&v)[E]) {
     const int64_t i = slice0 + (int64_t)r * ROW + lane * E;
     if (full) {
-      Chunk<T>::unpack(l2::ldg128_hint<NC>(p.in + i, pol), v);
+      Tin w[E];
+      Chunk<Tin>::unpack(l2::ldg128_hint<NC>(p.in + i, pol), w);
+#pragma unroll
+      for (int k = 0; k < E; ++k) v[k] = (T)w[k];
     } else {
 #pragma unroll
-      for (int k = 0; k < E; ++k) v[k] = i + k < p.n ? p.in[i + k] : neutral;
+      for (int k = 0; k < E; ++k) v[k] = i + k < p.n ? (T)p.in[i + k] : neutral;
     }
   };
 
@@ -414,7 +428,12 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T> p) {
       }
       const int64_t i = slice0 + (int64_t)(r0 + u) * ROW + lane * E;
       if (full) {
-        l2::stg128_hint(p.out + i, Chunk<T>::pack(o), drop);
+        if constexpr (WIDEN) {
+          const T lo[2] = {o[0], o[1]}, hi[2] = {o[2], o[3]};
+          l2::stg256_hint(p.out + i, Chunk<T>::pack(lo), Chunk<T>::pack(hi), drop);
+        } else {
+          l2::stg128_hint(p.out + i, Chunk<T>::pack(o), drop);
+        }
       } else {
 #pragma unroll
         for (int k = 0; k < E; ++k)
@@ -443,8 +462,8 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T> p) {
 // Register-tile fallback (arrays not 16-byte aligned): one tile of
 // BLOCK x ITEMS consecutive elements per CTA, scalar loads/stores.
 // ===========================================================================
-template <int OP, typename T, int BLOCK, int ITEMS, int DEPTH, bool EXCLUSIVE>
-__global__ void __launch_bounds__(BLOCK) scan_reg_kernel(ScanArgs<T> p) {
+template <int OP, typename T, typename Tin, int BLOCK, int ITEMS, int DEPTH, bool EXCLUSIVE>
+__global__ void __launch_bounds__(BLOCK) scan_reg_kernel(ScanArgs<T, Tin> p) {
   using O = Op<OP, T>;
   constexpr int WARPS = BLOCK / 32;
   constexpr int64_t TILE = (int64_t)BLOCK * ITEMS;
@@ -467,7 +486,7 @@ __global__ void __launch_bounds__(BLOCK) scan_reg_kernel(ScanArgs<T> p) {
 
   T x[ITEMS];
 #pragma unroll
-  for (int k = 0; k < ITEMS; ++k) x[k] = (i0 + k < p.n) ? p.in[i0 + k] : neutral;
+  for (int k = 0; k < ITEMS; ++k) x[k] = (i0 + k < p.n) ? (T)p.in[i0 + k] : neutral;
 #pragma unroll
   for (int k = 1; k < ITEMS; ++k) x[k] = O::fold(x[k - 1], x[k]);
   const T incl = warp_inclusive<OP, T>(x[ITEMS - 1], lane);
@@ -509,13 +528,13 @@ size_t status_bytes(int64_t tiles) {
 }
 
 // Fill the argument block for a tile size of tile_elems elements.
-template <typename T>
-ScanArgs<T> make_args(int64_t n, int64_t tile_elems, const void *in, void *out, const void *carry,
-                      int64_t carry_count, void *ws) {
-  ScanArgs<T> p;
+template <typename T, typename Tin = T>
+ScanArgs<T, Tin> make_args(int64_t n, int64_t tile_elems, const void *in, void *out, const void *carry,
+                           int64_t carry_count, void *ws) {
+  ScanArgs<T, Tin> p;
   p.n = n;
   p.num_tiles = (n + tile_elems - 1) / tile_elems;
-  p.in = static_cast<const T *>(in);
+  p.in = static_cast<const Tin *>(in);
   p.out = static_cast<T *>(out);
   p.carry = static_cast<const T *>(carry);
   p.carry_count = carry_count;

@@ -277,21 +277,28 @@ def min(x, out=None):  # noqa: A001
 
 
 # --------------------------------------------------------------- scan
-def scan(x, exclusive=False, out=None, carry=None, op=SUM):
+def scan(x, exclusive=False, out=None, carry=None, op=SUM, out_dtype=None):
     """Scan with reduction expression `op` (SUM / MAX / MIN) over int32,
-    int64 (wrapping), float32, float64 (PAPER.md:496-499).  `carry` is an
-    optional 1-D device tensor whose elements are all folded in front (a
+    int64 (wrapping), float32, float64 (PAPER.md:496-499).  `out_dtype`
+    (default x.dtype) may widen int32 -> int64 or float32 -> float64: the
+    scan then runs in the wide type (NEXT-2).  `carry` is an optional 1-D
+    device tensor of out_dtype whose elements are all folded in front (a
     sharded scan's offset)."""
     _check_array("x", x)
+    out_dtype = x.dtype if out_dtype is None else out_dtype
     if out is None:
-        out = torch.empty_like(x)
+        out = torch.empty(x.shape, dtype=out_dtype, device=x.device)
     else:
-        _same(x, out, "out")
-    dt = ga_dtype(x.dtype)
+        _check_array("out", out)
+        if out.shape != x.shape:
+            raise ValueError(f"out has length {out.numel()}, x has {x.numel()}")
+        if out.dtype != out_dtype or out.device != x.device:
+            raise TypeError(f"out must be a {out_dtype} tensor on {x.device}")
+    in_dt, dt = ga_dtype(x.dtype), ga_dtype(out_dtype)
     if carry is not None:
         _check_array("carry", carry)
-        if carry.dtype != x.dtype or carry.device != x.device:
-            raise TypeError("carry must match x's dtype and device")
+        if carry.dtype != out_dtype or carry.device != x.device:
+            raise TypeError("carry must match out_dtype and x's device")
         cptr, ccount = _ptr(carry), carry.numel()
     else:
         cptr, ccount = None, 0
@@ -299,7 +306,8 @@ def scan(x, exclusive=False, out=None, carry=None, op=SUM):
     nb = _abi.gpuarray_scan_workspace_bytes(dt, x.numel())
     w = workspace("scan", x.device, s, nb)
     kind = GA_SCAN_EXCLUSIVE if exclusive else GA_SCAN_INCLUSIVE
-    check(_abi.gpuarray_scan(op, kind, dt, x.numel(), _ptr(x), _ptr(out), cptr, ccount, w.data_ptr(), w.numel(), s))
+    check(_abi.gpuarray_scan(op, kind, in_dt, dt, x.numel(), _ptr(x), _ptr(out), cptr, ccount, w.data_ptr(),
+                             w.numel(), s))
     return out
 
 

@@ -38,7 +38,7 @@ def test_nm_shows_c_linkage(abi):
 
 
 def test_version_and_strings(abi):
-    assert abi.gpuarray_abi_version() == 2
+    assert abi.gpuarray_abi_version() == 3
     assert abi.gpuarray_status_string(abi.GA_OK) == "GA_OK"
     assert abi.gpuarray_status_string(abi.GA_ERR_CUDA) == "GA_ERR_CUDA"
     assert abi.gpuarray_status_string(99) == "GA_ERR_UNKNOWN"
@@ -81,14 +81,20 @@ def test_argument_validation_is_synchronous(abi):
     assert R(0, 0, 0, 0, 4, 4096, None, 64, None, ws, None) == abi.GA_ERR_WORKSPACE
     S = abi.gpuarray_scan
     sw = abi.gpuarray_scan_workspace_bytes(abi.GA_I32, 100)
-    assert S(5, 0, abi.GA_I32, 100, 4096, 8192, None, 0, 64, sw, None) == E                    # bad op
-    assert S(0, 0, 9, 100, 4096, 8192, None, 0, 64, sw, None) == E                            # bad dtype
-    assert S(0, 0, abi.GA_C64, 100, 4096, 8192, None, 0, 64, sw, None) == abi.GA_ERR_UNSUPPORTED  # complex scan
-    assert S(0, 3, abi.GA_I32, 100, 4096, 8192, None, 0, 64, sw, None) == E                   # bad kind
-    assert S(0, 0, abi.GA_I32, 100, 4096, 8192, None, 2, 64, sw, None) == E                   # carry NULL
-    assert S(0, 0, abi.GA_I32, 100, 4096, 4100, None, 0, 64, sw, None) == E                   # partial overlap
-    assert S(0, 0, abi.GA_I32, 100, 4096, 8192, None, 0, 64, sw - 1, None) == abi.GA_ERR_WORKSPACE
-    assert S(0, 0, abi.GA_I32, 0, None, None, None, 0, None, 0, None) == abi.GA_OK           # n == 0 no-op
+    I32, I64 = abi.GA_I32, abi.GA_I64
+    assert S(5, 0, I32, I32, 100, 4096, 8192, None, 0, 64, sw, None) == E                    # bad op
+    assert S(0, 0, 9, 9, 100, 4096, 8192, None, 0, 64, sw, None) == E                        # bad dtype
+    assert S(0, 0, abi.GA_C64, abi.GA_C64, 100, 4096, 8192, None, 0, 64, sw, None) == abi.GA_ERR_UNSUPPORTED
+    assert S(0, 0, I64, I32, 100, 4096, 8192, None, 0, 64, sw, None) == abi.GA_ERR_UNSUPPORTED  # narrowing
+    assert S(0, 0, I32, abi.GA_F64, 100, 4096, 8192, None, 0, 64, sw, None) == abi.GA_ERR_UNSUPPORTED
+    assert S(0, 3, I32, I32, 100, 4096, 8192, None, 0, 64, sw, None) == E                    # bad kind
+    assert S(0, 0, I32, I32, 100, 4096, 8192, None, 2, 64, sw, None) == E                    # carry NULL
+    assert S(0, 0, I32, I32, 100, 4096, 4100, None, 0, 64, sw, None) == E                    # partial overlap
+    sw64 = abi.gpuarray_scan_workspace_bytes(I64, 100)
+    assert S(0, 0, I32, I64, 100, 4096, 4096, None, 0, 64, sw64, None) == E                  # widening in place
+    assert "in place" in abi.gpuarray_last_error()
+    assert S(0, 0, I32, I32, 100, 4096, 8192, None, 0, 64, sw - 1, None) == abi.GA_ERR_WORKSPACE
+    assert S(0, 0, I32, I32, 0, None, None, None, 0, None, 0, None) == abi.GA_OK           # n == 0 no-op
 
 
 def test_python_error_mapping(abi):

@@ -418,6 +418,30 @@ def test_scan_float_sum_closed_forms():
     assert np.array_equal(oracle.scan(oracle.EXCLUSIVE, r), i * (i - 1) / 2)
 
 
+def test_scan_widening_closed_forms():
+    """Widened scans (R27): int32 -> int64 does not wrap where the int32 scan
+    does (closed form k*(2^31-1)); MAX/MIN are unchanged by widening; float32
+    -> float64 keeps prefixes an fp32 running sum loses (1 + k*2^-30)."""
+    n = 70_001
+    big = np.full(n, np.iinfo(np.int32).max, np.int32)
+    k = np.arange(1, n + 1, dtype=np.int64)
+    w = oracle.scan(oracle.INCLUSIVE, big, out_dtype=np.int64)
+    assert w.dtype == np.int64 and bits_equal(w, k * (2 ** 31 - 1))
+    we = oracle.scan(oracle.EXCLUSIVE, big, out_dtype=np.int64, carry=-5)
+    assert bits_equal(we, (k - 1) * (2 ** 31 - 1) - 5)
+    assert oracle.scan(oracle.INCLUSIVE, big)[1] == -2  # the narrow scan wraps: 2(2^31-1) mod 2^32
+    x = RNG.integers(-(1 << 31), (1 << 31) - 1, size=n, dtype=np.int32)
+    for op in (oracle.MAX, oracle.MIN):
+        assert bits_equal(oracle.scan(oracle.INCLUSIVE, x, op=op, out_dtype=np.int64),
+                          oracle.scan(oracle.INCLUSIVE, x, op=op).astype(np.int64))
+    f = np.full(1 << 16, 2.0 ** -30, np.float32)
+    f[0] = 1.0
+    pf = oracle.scan(oracle.INCLUSIVE, f, out_dtype=np.float64)
+    assert np.array_equal(pf, 1.0 + np.arange(1 << 16) * 2.0 ** -30)
+    with pytest.raises(TypeError):
+        oracle.scan(oracle.INCLUSIVE, np.zeros(3, np.int64), out_dtype=np.int32)
+
+
 # ------------------------------------------------------------ complex (NEXT-3)
 def _cplx(dt, n, seed):
     f = np.float32 if dt == np.complex64 else np.float64

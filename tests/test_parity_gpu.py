@@ -406,6 +406,57 @@ def test_scan_float_sum_within_bound(dt, exclusive, n):
         assert np.all(np.abs(got - ref) <= d * u * sa + 1e-300)
 
 
+# ------------------------------------------------------------------ widening scans (NEXT-2, R27)
+@pytest.mark.parametrize("op", [oracle.SUM, oracle.MAX, oracle.MIN])
+@pytest.mark.parametrize("exclusive", [False, True])
+@pytest.mark.parametrize("n", SCAN2_SIZES)
+def test_scan_widen_i32_i64_bit_exact(op, exclusive, n):
+    """int32 -> int64 scans: full-range data whose int32 SUM scan would wrap;
+    super-tile kernel (aligned), register kernel (unaligned input, and an
+    output that is 16- but not 32-byte aligned)."""
+    x = np.random.default_rng(n + 17).integers(-(1 << 31), (1 << 31) - 1, size=n, dtype=np.int32, endpoint=True)
+    kind = oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE
+    ref = oracle.scan(kind, x, op=op, out_dtype=np.int64)
+    for offs, out_offs in ((0, 0), (1, 0), (0, 2)):
+        out = torch.empty(n + out_offs, dtype=torch.int64, device=DEV)[out_offs:]
+        got = G.scan(to_dev(x, offs), exclusive=exclusive, op=op, out=out, out_dtype=torch.int64)
+        assert_bit_exact(got.cpu().numpy(), ref)
+
+
+def test_scan_widen_i32_i64_carry_and_errors():
+    n = 1_000_003
+    x = np.full(n, np.iinfo(np.int32).max, np.int32)
+    carry = np.array([-(1 << 40), 7], np.int64)
+    got = G.scan(to_dev(x), exclusive=True, carry=to_dev(carry), out_dtype=torch.int64).cpu().numpy()
+    assert_bit_exact(got, oracle.scan(oracle.EXCLUSIVE, x, carry=np.int64(-(1 << 40) + 7), out_dtype=np.int64))
+    assert int(got[-1]) == (n - 1) * (2 ** 31 - 1) - (1 << 40) + 7  # closed form, no wrap
+    xd = to_dev(x)
+    with pytest.raises(TypeError):
+        G.scan(xd, carry=to_dev(np.zeros(1, np.int32)), out_dtype=torch.int64)  # carry is out_dtype
+    with pytest.raises(TypeError):
+        G.scan(to_dev(x.astype(np.int64)), out_dtype=torch.int32)               # narrowing
+    with pytest.raises(ValueError):
+        G.scan(xd, out=torch.empty(n - 1, dtype=torch.int64, device=DEV), out_dtype=torch.int64)  # length
+
+
+@pytest.mark.parametrize("exclusive", [False, True])
+@pytest.mark.parametrize("n", [1, 4097, 1_000_003])
+def test_scan_widen_f32_f64_within_bound(exclusive, n):
+    """float32 -> float64 SUM scans: the f64 bound of R22 on the exact prefix
+    sums of the fp32 inputs; MAX/MIN bit-exact."""
+    x = host_data(np.float32, n, 8, signed=True)
+    kind = oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE
+    ref, sa = oracle.scan(kind, x, return_sumabs=True, out_dtype=np.float64)
+    d = np.arange(n) / 2048.0 + 512
+    for offs in (0, 1):
+        got = G.scan(to_dev(x, offs), exclusive=exclusive, out_dtype=torch.float64).cpu().numpy()
+        assert got.dtype == np.float64
+        assert np.all(np.abs(got - ref) <= d * 2.0 ** -53 * sa + 1e-300)
+        for op in (oracle.MAX, oracle.MIN):
+            g2 = G.scan(to_dev(x, offs), exclusive=exclusive, op=op, out_dtype=torch.float64).cpu().numpy()
+            assert_bit_exact(g2, oracle.scan(kind, x, op=op, out_dtype=np.float64))
+
+
 # ------------------------------------------------------------------ complex (NEXT-3)
 CPLX = {np.complex64: torch.complex64, np.complex128: torch.complex128}
 

@@ -69,7 +69,9 @@ def test_vector_widths(sass):
             assert re.search(r"LDG\.E\S*\.256", body), d
             seen["red"] = True
         if "scan_l2_kernel" in d:
-            assert re.search(r"LDG\.E\S*\.128", body) and re.search(r"STG\.E\S*\.128", body), d
+            widen = "ScanArgs<double, float>" in d or "ScanArgs<long, int>" in d
+            st = r"STG\.E\S*\.256" if widen else r"STG\.E\S*\.128"  # widened rows: 32 B per lane
+            assert re.search(r"LDG\.E\S*\.128", body) and re.search(st, body), d
             seen["scan"] = True
     assert all(seen.values()), seen
 

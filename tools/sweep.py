@@ -48,12 +48,13 @@ def main():
         ("norm2", torch.float32, 4), ("norm2", torch.float64, 8),
         ("dot", torch.float32, 8), ("sum", torch.float32, 4),
         ("scan", torch.int32, 8), ("scan", torch.int64, 16),
+        ("scan_widen", torch.int32, 12),  # int32 in, int64 out (NEXT-2)
     ]
     for lg in range(a.min, a.max + 1):
         n = 1 << lg
         for name, dt, bpe in ops:
             esz = torch.tensor([], dtype=dt).element_size()
-            need = 3 * n * esz if name == "axpbyz" else 2 * n * esz
+            need = 3 * n * esz if name in ("axpbyz", "scan_widen") else 2 * n * esz
             if need > torch.cuda.mem_get_info()[0] * 0.8:
                 continue
             if dt.is_floating_point:
@@ -64,7 +65,7 @@ def main():
                 kind = synth.I32_RANGE if dt == torch.int32 else synth.I64_RANGE
                 x = synth.device_fill(kind, 3, n, lo=0, hi=9, device=dev)
                 y = None
-            out = torch.empty_like(x)
+            out = torch.empty(n, dtype=torch.int64, device=dev) if name == "scan_widen" else torch.empty_like(x)
             r = torch.empty((), dtype=dt, device=dev)
             fn = {
                 "axpbyz": lambda: G.axpbyz(5.0, x, 6.0, y, out=out),
@@ -72,6 +73,7 @@ def main():
                 "dot": lambda: G.dot(x, y, out=r),
                 "sum": lambda: G.sum(x, out=r),
                 "scan": lambda: G.scan(x, exclusive=True, out=out),
+                "scan_widen": lambda: G.scan(x, exclusive=True, out=out, out_dtype=torch.int64),
             }[name]
             small = need < 4 * L2_BYTES
             for _ in range(3):
