@@ -6,6 +6,8 @@
 // One launch, decoupled look-back across super-tiles (BASELINE.json
 // north_star), HBM traffic 1 read + 1 write per element when the super-tiles
 // in flight stay L2-resident (scan_l2_kernel in scan_kernel.cuh):
+// The super-tile shape is chosen by size (scan_impl.cuh: smaller tiles for
+// small n so every SM gets work); described here for the streaming shape L:
 //   - CTA draws {epoch, super-tile id} with one 64-bit atomic (ids in CTA
 //     start order, so every predecessor is already running);
 //   - phase 1 streams its 384 KiB super-tile from HBM (each of 24 warps its
@@ -26,82 +28,24 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include <algorithm>
-
-#include "ga_host.h"
-#include "scan_kernel.cuh"
+#include "scan_impl.cuh"
 
 namespace ga {
+namespace scan_impl {
+GA_SCAN_INSTANTIATE(SHAPE_RG)
+}  // namespace scan_impl
+
+using namespace scan_impl;
+
 namespace {
-
-using namespace scan_detail;
-
-// Tuned super-tile shape (tools/lab/run_scan_lab.py): 24 warps x 32 rows of
-// 512 bytes = 384 KiB per CTA (one CTA per SM), 8 rows in flight per warp,
-// 8-deep look-back (256 predecessors per round trip), and warps 1..23 load
-// and locally scan their first phase-3 rows while warp 0 looks back.
-constexpr int L2_WARPS = 24, L2_ROWS = 32, L2_UNROLL = 8, L2_DEPTH = 8;
-// Fallback for arrays that are not 16-byte aligned: register tile of
-// 256 threads x 16 scalar-loaded items.
-constexpr int RG_BLOCK = 256, RG_ITEMS = 16, RG_DEPTH = 4;
-
-template <typename T>
-constexpr int64_t l2_tile() {
-  return (int64_t)L2_WARPS * L2_ROWS * 512 / (int64_t)sizeof(T);
-}
-
 template <typename T>
 size_t ws_bytes(int64_t n) {
-  // status for the smaller of the two tile sizes (either path may run)
-  const int64_t min_tile = std::min<int64_t>(l2_tile<T>(), (int64_t)RG_BLOCK * RG_ITEMS);
-  return HEADER + status_bytes<T>(cdiv(n, min_tile));
+  // status for the smallest tile any path may use (the RG fallback's; every
+  // super-tile shape has at least as many elements, also widened)
+  static_assert(tile_elems<SHAPE_S, int32_t, int32_t>() >= tile_elems<SHAPE_RG, T, T>(), "RG tile is the smallest");
+  static_assert(tile_elems<SHAPE_S, int64_t, int64_t>() >= tile_elems<SHAPE_RG, T, T>(), "RG tile is the smallest");
+  return HEADER + status_bytes<T>(cdiv(n, tile_elems<SHAPE_RG, T, T>()));
 }
-
-// Tin != T: the widened scans (int32 -> int64, float -> double; NEXT-2),
-// same kernels, the input converted on load; a widened row stores 32 bytes
-// per lane, so the super-tile path needs a 32-byte aligned output.
-template <int OP, typename T, typename Tin, bool EXCLUSIVE>
-ga_status_t run(int64_t n, const void *in, void *out, const void *carry, int64_t carry_count, void *ws,
-                cudaStream_t s) {
-  constexpr uintptr_t OUT_ALIGN = sizeof(T) == sizeof(Tin) ? 16 : 32;
-  const bool aligned = ((uintptr_t)in & 15) == 0 && ((uintptr_t)out & (OUT_ALIGN - 1)) == 0;
-  const bool inplace = in == out;
-  if (aligned) {
-    ScanArgs<T, Tin> p = make_args<T, Tin>(n, l2_tile<Tin>(), in, out, carry, carry_count, ws);
-    const int grid = (int)p.num_tiles;
-    if (inplace)
-      scan_l2_kernel<OP, T, Tin, L2_WARPS, L2_ROWS, L2_UNROLL, L2_DEPTH, false, EXCLUSIVE, true>
-          <<<grid, L2_WARPS * 32, 0, s>>>(p);
-    else
-      scan_l2_kernel<OP, T, Tin, L2_WARPS, L2_ROWS, L2_UNROLL, L2_DEPTH, true, EXCLUSIVE, true>
-          <<<grid, L2_WARPS * 32, 0, s>>>(p);
-  } else {
-    ScanArgs<T, Tin> p = make_args<T, Tin>(n, (int64_t)RG_BLOCK * RG_ITEMS, in, out, carry, carry_count, ws);
-    if (p.num_tiles > 0x7fffffffLL) return fail(GA_ERR_UNSUPPORTED, "scan: n too large (%lld)", (long long)n);
-    scan_reg_kernel<OP, T, Tin, RG_BLOCK, RG_ITEMS, RG_DEPTH, EXCLUSIVE><<<(int)p.num_tiles, RG_BLOCK, 0, s>>>(p);
-  }
-  count_launch();
-  return check_launch("scan_kernel");
-}
-
-template <int OP, typename T, typename Tin>
-ga_status_t by_kind(bool ex, int64_t n, const void *in, void *out, const void *carry, int64_t cc, void *ws,
-                    cudaStream_t s) {
-  return ex ? run<OP, T, Tin, true>(n, in, out, carry, cc, ws, s)
-            : run<OP, T, Tin, false>(n, in, out, carry, cc, ws, s);
-}
-
-template <typename T, typename Tin = T>
-ga_status_t by_op(ga_op_t op, bool ex, int64_t n, const void *in, void *out, const void *carry, int64_t cc, void *ws,
-                  cudaStream_t s) {
-  switch (op) {
-    case GA_OP_SUM: return by_kind<GA_OP_SUM, T, Tin>(ex, n, in, out, carry, cc, ws, s);
-    case GA_OP_MAX: return by_kind<GA_OP_MAX, T, Tin>(ex, n, in, out, carry, cc, ws, s);
-    case GA_OP_MIN: return by_kind<GA_OP_MIN, T, Tin>(ex, n, in, out, carry, cc, ws, s);
-  }
-  return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad op %d", (int)op);
-}
-
 }  // namespace
 
 size_t scan_workspace_bytes(ga_dtype_t dt, int64_t n) {
@@ -117,19 +61,15 @@ size_t scan_workspace_bytes(ga_dtype_t dt, int64_t n) {
 ga_status_t launch_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t in_dt, ga_dtype_t dt, int64_t n, const void *in,
                         void *out, const void *carry, int64_t carry_count, void *ws, cudaStream_t s) {
   const bool ex = kind == GA_SCAN_EXCLUSIVE;
-  if (in_dt != dt) {
-    if (in_dt == GA_I32 && dt == GA_I64) return by_op<int64_t, int32_t>(op, ex, n, in, out, carry, carry_count, ws, s);
-    if (in_dt == GA_F32 && dt == GA_F64) return by_op<double, float>(op, ex, n, in, out, carry, carry_count, ws, s);
-    return fail(GA_ERR_UNSUPPORTED, "scan %d -> %d not instantiated", (int)in_dt, (int)dt);
+  const size_t isz = dtype_size(in_dt), osz = dtype_size(dt);
+  const uintptr_t out_align = isz == osz ? 16 : 32;
+  const bool aligned = ((uintptr_t)in & 15) == 0 && ((uintptr_t)out & (out_align - 1)) == 0;
+  if (!aligned) return launch_shape<SHAPE_RG>(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);
+  switch (choose_shape(n, isz, osz)) {
+    case SHAPE_S: return launch_shape<SHAPE_S>(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);
+    case SHAPE_M: return launch_shape<SHAPE_M>(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);
+    default: return launch_shape<SHAPE_L>(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);
   }
-  switch (dt) {
-    case GA_I32: return by_op<int32_t>(op, ex, n, in, out, carry, carry_count, ws, s);
-    case GA_I64: return by_op<int64_t>(op, ex, n, in, out, carry, carry_count, ws, s);
-    case GA_F32: return by_op<float>(op, ex, n, in, out, carry, carry_count, ws, s);
-    case GA_F64: return by_op<double>(op, ex, n, in, out, carry, carry_count, ws, s);
-    default: break;
-  }
-  return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad dtype %d", (int)dt);
 }
 
 }  // namespace ga

@@ -352,30 +352,38 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p)
   const uint64_t keep = l2::policy_evict_last();
   const uint64_t drop = l2::policy_evict_first();
 
-  auto load_row = [&](int r, uint64_t pol, T (&v)[E]) {
+  // A row stays in registers as its raw 16 input bytes (4 registers for
+  // every T / Tin); it is unpacked and widened only where it is folded, so
+  // the 8-byte and widened scans hold no more live state than int32.
+  auto load_raw = [&](int r, uint64_t pol) -> uint4 {
     const int64_t i = slice0 + (int64_t)r * ROW + lane * E;
-    if (full) {
-      Tin w[E];
-      Chunk<Tin>::unpack(l2::ldg128_hint<NC>(p.in + i, pol), w);
+    if (full) return l2::ldg128_hint<NC>(p.in + i, pol);
+    Tin e[E];  // ragged tail: padding only reaches positions >= n (never stored)
 #pragma unroll
-      for (int k = 0; k < E; ++k) v[k] = (T)w[k];
-    } else {
+    for (int k = 0; k < E; ++k) e[k] = i + k < p.n ? p.in[i + k] : Op<OP, Tin>::neutral();
+    return Chunk<Tin>::pack(e);
+  };
+  auto widen = [&](const uint4 &raw, T (&v)[E]) {
+    Tin e[E];
+    Chunk<Tin>::unpack(raw, e);
 #pragma unroll
-      for (int k = 0; k < E; ++k) v[k] = i + k < p.n ? (T)p.in[i + k] : neutral;
-    }
+    for (int k = 0; k < E; ++k) v[k] = (T)e[k];
   };
 
   // phase 1: slice folds
   T acc = neutral;
 #pragma unroll 1
   for (int r0 = 0; r0 < ROWS; r0 += UNROLL) {
-    T v[UNROLL][E];
+    uint4 raw[UNROLL];
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) load_row(r0 + u, keep, v[u]);
+    for (int u = 0; u < UNROLL; ++u) raw[u] = load_raw(r0 + u, keep);
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u)
+    for (int u = 0; u < UNROLL; ++u) {
+      T v[E];
+      widen(raw[u], v);
 #pragma unroll
-      for (int k = 0; k < E; ++k) acc = O::fold(acc, v[u][k]);
+      for (int k = 0; k < E; ++k) acc = O::fold(acc, v[k]);
+    }
   }
   acc = warp_fold<OP, T>(acc);
   if (lane == 0) s_slice[warp] = acc;
@@ -400,31 +408,38 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p)
     if (lane < WARPS) s_slice[lane] = O::fold(prefix, wex);  // exclusive prefix of slice `lane`
   }
 
-  // phase 3 helpers.  load_local: rows [r0, r0+UNROLL) into registers,
-  // in-row scans, each row's exclusive offset relative to the chunk start
-  // (off) and the chunk fold (ctot).
-  auto load_local = [&](int r0, T (&v)[UNROLL][E], T (&off)[UNROLL], T &ctot) {
+  // phase 3 helpers.  load_local: rows [r0, r0+UNROLL) into registers (raw),
+  // each row's exclusive offset relative to the chunk start (off: the
+  // warp-exclusive scan of the lanes' in-lane folds) and the chunk fold
+  // (ctot).  store_chunk redoes the in-lane running fold v0 ⊕ .. ⊕ vk — the
+  // same operations in the same order, so results do not change.
+  auto load_local = [&](int r0, uint4 (&raw)[UNROLL], T (&off)[UNROLL], T &ctot) {
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) load_row(r0 + u, drop, v[u]);
+    for (int u = 0; u < UNROLL; ++u) raw[u] = load_raw(r0 + u, drop);
     ctot = neutral;
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
+      T v[E];
+      widen(raw[u], v);
 #pragma unroll
-      for (int k = 1; k < E; ++k) v[u][k] = O::fold(v[u][k - 1], v[u][k]);
-      const T x = warp_inclusive<OP, T>(v[u][E - 1], lane);
+      for (int k = 1; k < E; ++k) v[k] = O::fold(v[k - 1], v[k]);
+      const T x = warp_inclusive<OP, T>(v[E - 1], lane);
       off[u] = O::fold(ctot, warp_exclusive_of<OP, T>(x, lane));
       ctot = O::fold(ctot, __shfl_sync(0xffffffffu, x, 31));
     }
   };
-  auto store_chunk = [&](int r0, const T (&v)[UNROLL][E], const T (&off)[UNROLL], T base) {
+  auto store_chunk = [&](int r0, const uint4 (&raw)[UNROLL], const T (&off)[UNROLL], T base) {
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
       const T cb = O::fold(base, off[u]);
-      T o[E];
+      T v[E], o[E];
+      widen(raw[u], v);
+#pragma unroll
+      for (int k = 1; k < E; ++k) v[k] = O::fold(v[k - 1], v[k]);
 #pragma unroll
       for (int k = 0; k < E; ++k) {
-        if constexpr (EXCLUSIVE) o[k] = k == 0 ? cb : O::fold(cb, v[u][k - 1]);
-        else o[k] = O::fold(cb, v[u][k]);
+        if constexpr (EXCLUSIVE) o[k] = k == 0 ? cb : O::fold(cb, v[k - 1]);
+        else o[k] = O::fold(cb, v[k]);
       }
       const int64_t i = slice0 + (int64_t)(r0 + u) * ROW + lane * E;
       if (full) {
@@ -441,7 +456,8 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p)
       }
     }
   };
-  T v0[UNROLL][E], off0[UNROLL], ctot0;
+  uint4 v0[UNROLL];
+  T off0[UNROLL], ctot0;
   const bool early = EARLY && warp != 0;
   if (early) load_local(0, v0, off0, ctot0);
   __syncthreads();
@@ -451,7 +467,8 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p)
   base = O::fold(base, ctot0);
 #pragma unroll 1
   for (int r0 = UNROLL; r0 < ROWS; r0 += UNROLL) {
-    T v[UNROLL][E], off[UNROLL], ctot;
+    uint4 v[UNROLL];
+    T off[UNROLL], ctot;
     load_local(r0, v, off, ctot);
     store_chunk(r0, v, off, base);
     base = O::fold(base, ctot);

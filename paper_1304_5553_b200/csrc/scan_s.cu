@@ -1,0 +1,8 @@
+// scan_s.cu — the S super-tile shape of the scans (see scan_impl.cuh).
+#include "scan_impl.cuh"
+
+namespace ga {
+namespace scan_impl {
+GA_SCAN_INSTANTIATE(SHAPE_S)
+}  // namespace scan_impl
+}  // namespace ga

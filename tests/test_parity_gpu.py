@@ -406,6 +406,27 @@ def test_scan_float_sum_within_bound(dt, exclusive, n):
         assert np.all(np.abs(got - ref) <= d * u * sa + 1e-300)
 
 
+# ------------------------------------------------------------------ scan super-tile shapes
+# (scan_impl.cuh: L when it gives >= 256 tiles, else M when >= 64, else S;
+# tiles of 24x32 / 32x8 / 8x8 (16x8 for 8-byte T) rows of 512 input bytes)
+def _shape_sizes(isz, osz):
+    tile = {"S": (16 if osz == 8 else 8) * 8 * 512 // isz, "M": 32 * 8 * 512 // isz, "L": 24 * 32 * 512 // isz}
+    return [64 * tile["M"] - 1, 64 * tile["M"] + 77, 256 * tile["L"] - 3, 256 * tile["L"] + 1001]
+
+
+@pytest.mark.parametrize("pair", [(np.int32, np.int32), (np.int64, np.int64), (np.int32, np.int64)])
+@pytest.mark.parametrize("exclusive", [False, True])
+def test_scan_shape_boundaries(pair, exclusive):
+    """Sizes either side of the S/M and M/L switch points, wrapping data."""
+    tin, tout = pair
+    kind = oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE
+    for n in _shape_sizes(np.dtype(tin).itemsize, np.dtype(tout).itemsize):
+        info = np.iinfo(tin)
+        x = np.random.default_rng(n).integers(info.min, info.max, size=n, dtype=tin, endpoint=True)
+        got = G.scan(to_dev(x), exclusive=exclusive, out_dtype=NPT[tout]).cpu().numpy()
+        assert_bit_exact(got, oracle.scan(kind, x, out_dtype=tout))
+
+
 # ------------------------------------------------------------------ widening scans (NEXT-2, R27)
 @pytest.mark.parametrize("op", [oracle.SUM, oracle.MAX, oracle.MIN])
 @pytest.mark.parametrize("exclusive", [False, True])
