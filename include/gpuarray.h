@@ -19,6 +19,12 @@
  *   gpuarray_scan                      parallel prefix sum, §3.2.6
  *       "GPU-based parallel prefix sums".
  *
+ * Beyond them: the other GPUArray operators and cumath maps
+ * (gpuarray_elementwise), device-scalar coefficients (gpuarray_axpbyz_ds),
+ * the fused cross-GPU finish (gpuarray_reduce_xgpu), and the CG workload's
+ * operator and fused iteration steps (gpuarray_stencil3, gpuarray_cg_direction,
+ * gpuarray_cg_update; the paper's Krylov solver).
+ *
  * Conventions (all entry points):
  *   - Pointers x, y, z, in, out, carry, workspace are DEVICE pointers on the
  *     current CUDA device; `stream` is a cudaStream_t (NULL = legacy default
@@ -45,7 +51,7 @@
 extern "C" {
 #endif
 
-#define GPUARRAY_ABI_VERSION 3
+#define GPUARRAY_ABI_VERSION 4
 
 /* C64 / C128: complex numbers as interleaved (re, im) float / double pairs
  * ("seamless support for complex numbers"; §8(f) NEXT-3). */
@@ -227,6 +233,38 @@ ga_status_t gpuarray_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t in_dt, ga_
  * 1-D Poisson: l = u = -1, d = 2. */
 ga_status_t gpuarray_stencil3(ga_dtype_t dt, int64_t n, ga_scalar_t l, ga_scalar_t d, ga_scalar_t u,
                               const void *diag, const void *x, void *y, void *stream);
+
+/* ---- The two fused steps of one CG iteration (NEXT-4).
+ * Each is ONE kernel doing what three of the calls above do, with the same
+ * per-element rounding, so an iteration is 2 launches and 10 element-sizes of
+ * HBM traffic instead of 6 and 14 (R28).  dt in {F32, F64}
+ * (others GA_ERR_UNSUPPORTED).  Scalar factors are ga_dscalar_t (device
+ * factors read when the kernel runs: graph-capturable).  The workspace is a
+ * gpuarray_reduce workspace (gpuarray_reduce_workspace_bytes(dt, n), zeroed
+ * once; not shared by calls in flight at the same time).  n == 0 writes 0 to
+ * the scalar result.
+ *
+ * gpuarray_cg_direction:
+ *   beta    = RN(beta.scale * RN(*beta.num / *beta.den))  (ga_dscalar_t)
+ *   p_out_i = RN(r_i + RN(beta * p_in_i))                  (= gpuarray_axpbyz(1, r, beta, p_in))
+ *   ap_i    = (A p_out)_i, A = tridiag(l, d_i, u)          (= gpuarray_stencil3, R25; d_i = diag[i] if diag)
+ *   *pap    = sum_i p_out_i * ap_i                          (dot, tolerance R9/R10)
+ * r, p_in, diag: n elements, read only; p_out, ap: n elements written; p_out
+ * and ap must not overlap each other or any input (neighbours are read);
+ * pap: one device element of dt. */
+ga_status_t gpuarray_cg_direction(ga_dtype_t dt, int64_t n, ga_dscalar_t beta, const void *r, const void *p_in,
+                                  void *p_out, ga_scalar_t l, ga_scalar_t d, ga_scalar_t u, const void *diag, void *ap,
+                                  void *pap, void *workspace, size_t workspace_bytes, void *stream);
+
+/* gpuarray_cg_update:
+ *   alpha = RN(alpha.scale * RN(*alpha.num / *alpha.den))
+ *   x_i  <- RN(x_i + RN(alpha * p_i))                       (= gpuarray_axpbyz_ds(1, x, alpha, p))
+ *   r_i  <- RN(r_i + RN(-alpha * ap_i))                     (= gpuarray_axpbyz_ds(1, r, -alpha, ap))
+ *   *rr   = sum_i r_i^2 of the updated r                    (norm2sq, tolerance R9/R10)
+ * x, r: n elements updated in place; p, ap: n elements read; the four must
+ * not overlap; rr: one device element of dt. */
+ga_status_t gpuarray_cg_update(ga_dtype_t dt, int64_t n, ga_dscalar_t alpha, void *x, void *r, const void *p,
+                               const void *ap, void *rr, void *workspace, size_t workspace_bytes, void *stream);
 
 /* Static strings; never NULL. */
 const char *gpuarray_status_string(ga_status_t status);

@@ -22,7 +22,8 @@ EXPORTS = (
     "gpuarray_axpbyz", "gpuarray_axpbz", "gpuarray_reduce_workspace_bytes", "gpuarray_reduce",
     "gpuarray_scan_workspace_bytes", "gpuarray_scan", "gpuarray_status_string", "gpuarray_last_error",
     "gpuarray_abi_version", "gpuarray_launch_count", "gpuarray_xgpu_buffer_bytes", "gpuarray_reduce_xgpu",
-    "gpuarray_stencil3", "gpuarray_axpbyz_ds", "gpuarray_elementwise",
+    "gpuarray_stencil3", "gpuarray_axpbyz_ds", "gpuarray_elementwise", "gpuarray_cg_direction",
+    "gpuarray_cg_update",
 )
 
 
@@ -119,6 +120,11 @@ def _load():
     lib.gpuarray_axpbyz_ds.argtypes = [st, i64, ga_dscalar_t, vp, ga_dscalar_t, vp, vp, vp]
     lib.gpuarray_stencil3.restype = st
     lib.gpuarray_stencil3.argtypes = [st, i64, ga_scalar_t, ga_scalar_t, ga_scalar_t, vp, vp, vp, vp]
+    lib.gpuarray_cg_direction.restype = st
+    lib.gpuarray_cg_direction.argtypes = [st, i64, ga_dscalar_t, vp, vp, vp, ga_scalar_t, ga_scalar_t, ga_scalar_t, vp,
+                                          vp, vp, vp, sz, vp]
+    lib.gpuarray_cg_update.restype = st
+    lib.gpuarray_cg_update.argtypes = [st, i64, ga_dscalar_t, vp, vp, vp, vp, vp, vp, sz, vp]
     return lib
 
 
@@ -212,3 +218,12 @@ def check(status):
     if status == GA_ERR_UNSUPPORTED:
         raise TypeError(msg)
     raise GpuArrayError(status, detail)
+
+
+def gpuarray_cg_direction(dt, n, beta, r, p_in, p_out, l, d, u, diag, ap, pap, workspace, workspace_bytes, stream):
+    return LIB.gpuarray_cg_direction(dt, n, beta, r, p_in, p_out, l, d, u, diag, ap, pap, workspace, workspace_bytes,
+                                     stream)
+
+
+def gpuarray_cg_update(dt, n, alpha, x, r, p, ap, rr, workspace, workspace_bytes, stream):
+    return LIB.gpuarray_cg_update(dt, n, alpha, x, r, p, ap, rr, workspace, workspace_bytes, stream)

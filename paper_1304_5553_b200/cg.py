@@ -61,23 +61,29 @@ def cg(b, offdiag=-1.0, d=2.0, diag=None, x0=None, rtol=1e-10, maxiter=None):
 
 class GraphCG:
     """CG with every scalar left on the GPU: alpha = rs/pAp and beta =
-    rs_new/rs enter the axpbyz kernels as device-resident factors
-    (gpuarray_axpbyz_ds), so `block` iterations (an even number) are captured
-    ONCE in a CUDA graph at construction and replayed by every solve(); the
-    host reads the residual only between blocks.  Iteration counts are
-    rounded up to whole blocks (a zero numerator keeps a converged iteration
-    finite, see ga_dscalar_t)."""
+    rs_new/rs enter the kernels as device-resident factors (ga_dscalar_t), so
+    `block` iterations (an even number) are captured ONCE in a CUDA graph at
+    construction and replayed by every solve(); the host reads the residual
+    only between blocks.  Iteration counts are rounded up to whole blocks (a
+    zero numerator keeps a converged iteration finite, see ga_dscalar_t).
 
-    def __init__(self, n, dtype=torch.float64, offdiag=-1.0, d=2.0, diag=None, block=16, device=None):
+    fused=True (default): two kernels per iteration, gpuarray_cg_direction
+    (p = r + beta p; Ap; p.Ap) and gpuarray_cg_update (x += alpha p;
+    r -= alpha Ap; r.r) — 10 element-sizes of HBM traffic per iteration.
+    fused=False: the six single-operation kernels (stencil3, dot, three
+    axpbyz_ds, norm2sq) — 14 element-sizes."""
+
+    def __init__(self, n, dtype=torch.float64, offdiag=-1.0, d=2.0, diag=None, block=16, device=None, fused=True):
         if block < 2 or block % 2:
             raise ValueError("block must be an even number >= 2")
         if dtype not in (torch.float32, torch.float64):
             raise TypeError("GraphCG needs float32 or float64")
         dev = torch.device(device or "cuda")
-        self.n, self.block, self.dev = n, block, dev
+        self.n, self.block, self.dev, self.fused = n, block, dev, fused
         self.offdiag, self.d, self.diag = offdiag, d, diag
         mk = lambda: torch.zeros(n, dtype=dtype, device=dev)  # noqa: E731
         self.b, self.x, self.r, self.p, self.ap = mk(), mk(), mk(), mk(), mk()
+        self.p2 = [self.p, mk()] if fused else None  # fused: p ping-pongs (neighbours are read)
         self.rs = [torch.zeros(1, dtype=dtype, device=dev) for _ in range(2)]
         self.pap = torch.zeros(1, dtype=dtype, device=dev)
         self.stream = torch.cuda.Stream(dev)
@@ -96,10 +102,17 @@ class GraphCG:
     def _start(self):
         G.stencil3(self.offdiag, self.d, self.offdiag, self.x, diag=self.diag, out=self.ap)
         G.axpbyz(1.0, self.b, -1.0, self.ap, out=self.r)
-        G.axpbz(1.0, self.r, -0.0, out=self.p)
         G.reduce(G.SUM, G.SQUARE, self.r, out=self.rs[0])
+        if self.fused:
+            # iteration 0 forms p = r + beta*0 with beta = rs0 / 1 (finite)
+            self.p2[1].zero_()
+            self.rs[1].fill_(1.0)
+        else:
+            G.axpbz(1.0, self.r, -0.0, out=self.p)
 
     def _iteration(self, k):
+        if self.fused:
+            return self._iteration_fused(k)
         cur, nxt = self.rs[k & 1], self.rs[(k + 1) & 1]
         x, r, p, ap, pap = self.x, self.r, self.p, self.ap, self.pap
         G.stencil3(self.offdiag, self.d, self.offdiag, p, diag=self.diag, out=ap)
@@ -108,6 +121,14 @@ class GraphCG:
         G.axpbyz_ds(1.0, r, -1.0, ap, out=r, b_num=cur, b_den=pap)    # r -= (rs/pAp) Ap
         G.reduce(G.SUM, G.SQUARE, r, out=nxt)                          # rs_new
         G.axpbyz_ds(1.0, r, 1.0, p, out=p, b_num=nxt, b_den=cur)      # p = r + (rs_new/rs) p
+
+    def _iteration_fused(self, k):
+        cur, prev = self.rs[k & 1], self.rs[(k + 1) & 1]
+        pin, pout = self.p2[(k + 1) & 1], self.p2[k & 1]
+        G.cg_direction(self.r, pin, pout, self.ap, beta=1.0, beta_num=cur, beta_den=prev, l=self.offdiag, d=self.d,
+                       u=self.offdiag, diag=self.diag, out=self.pap)               # p = r + (rs/rs_prev) p; Ap; p.Ap
+        G.cg_update(self.x, self.r, pout, self.ap, alpha=1.0, alpha_num=cur, alpha_den=self.pap,
+                    out=prev)                                                     # x, r update; rs_new -> rs[(k+1)&1]
 
     def solve(self, b, x0=None, rtol=1e-10, maxiter=None):
         G._check_array("b", b)
@@ -137,8 +158,8 @@ class GraphCG:
         return CGResult(self.x.clone(), k, hist, conv)
 
 
-def cg_graph(b, offdiag=-1.0, d=2.0, diag=None, x0=None, rtol=1e-10, maxiter=None, block=16):
+def cg_graph(b, offdiag=-1.0, d=2.0, diag=None, x0=None, rtol=1e-10, maxiter=None, block=16, fused=True):
     """One-shot convenience wrapper around GraphCG (captures a graph per call;
     build a GraphCG once to solve repeatedly)."""
-    solver = GraphCG(b.numel(), b.dtype, offdiag, d, diag, block, b.device)
+    solver = GraphCG(b.numel(), b.dtype, offdiag, d, diag, block, b.device, fused=fused)
     return solver.solve(b, x0=x0, rtol=rtol, maxiter=maxiter)

@@ -42,20 +42,6 @@ struct EwArgs {
   const T *an = nullptr, *ad = nullptr, *bn = nullptr, *bd = nullptr;
 };
 
-template <typename T>
-__device__ __forceinline__ T coef(T scale, const T *num, const T *den) {
-  if constexpr (std::is_floating_point<T>::value) {
-    if (!num && !den) return scale;
-    const T nv = num ? *num : T(1);
-    // a zero numerator gives a zero factor whatever the denominator (a
-    // converged CG iteration has 0/0 and must stay finite)
-    const T q = nv == T(0) ? T(0) : (den ? e_div(nv, *den) : nv);
-    return e_mul(scale, q);
-  } else {
-    return scale;
-  }
-}
-
 // One element of the statement; the rounding sequence is DESIGN.md R1.
 template <typename T, bool HAS_Y>
 __device__ __forceinline__ T stmt(T a, T x, T b, T y) {

@@ -240,4 +240,20 @@ __device__ __forceinline__ T warp_fold(T v) {
   return v;
 }
 
+// Coefficient with a device-resident factor (ga_dscalar_t): RN(scale *
+// RN(num / den)), a missing pointer standing for 1, both missing: scale.  A
+// zero numerator gives a zero factor whatever the denominator (a converged CG
+// iteration has 0/0 and must stay finite).
+template <typename T>
+__device__ __forceinline__ T coef(T scale, const T *num, const T *den) {
+  if constexpr (std::is_floating_point<T>::value) {
+    if (!num && !den) return scale;
+    const T nv = num ? *num : T(1);
+    const T q = nv == T(0) ? T(0) : (den ? e_div(nv, *den) : nv);
+    return e_mul(scale, q);
+  } else {
+    return scale;
+  }
+}
+
 }  // namespace ga

@@ -66,6 +66,11 @@ ga_status_t launch_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t in_dt, ga_dt
 ga_status_t launch_stencil3(ga_dtype_t dt, int64_t n, const ga_scalar_t &l, const ga_scalar_t &d,
                             const ga_scalar_t &u, const void *diag, const void *x, void *y, cudaStream_t s);
 
+ga_status_t launch_cg_direction(ga_dtype_t dt, int64_t n, const ga_dscalar_t &beta, const void *r, const void *pin,
+                                void *pout, const ga_scalar_t &l, const ga_scalar_t &d, const ga_scalar_t &u,
+                                const void *diag, void *ap, void *pap, void *ws, cudaStream_t s);
+ga_status_t launch_cg_update(ga_dtype_t dt, int64_t n, const ga_dscalar_t &alpha, void *x, void *r, const void *p,
+                             const void *ap, void *rr, void *ws, cudaStream_t s);
 bool ewop_binary(ga_ewop_t op);
 ga_status_t launch_ewmap(ga_ewop_t op, ga_dtype_t dt, int64_t n, const void *x, const void *y, void *z,
                          cudaStream_t s);

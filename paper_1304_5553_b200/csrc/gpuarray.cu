@@ -224,6 +224,49 @@ ga_status_t gpuarray_stencil3(ga_dtype_t dt, int64_t n, ga_scalar_t l, ga_scalar
   return launch_stencil3(dt, n, l, d, u, diag, x, y, (cudaStream_t)stream);
 }
 
+static bool overlaps(const void *p, const void *q, size_t bytes) {
+  return p && q && (uintptr_t)p < (uintptr_t)q + bytes && (uintptr_t)q < (uintptr_t)p + bytes;
+}
+
+ga_status_t gpuarray_cg_direction(ga_dtype_t dt, int64_t n, ga_dscalar_t beta, const void *r, const void *p_in,
+                                  void *p_out, ga_scalar_t l, ga_scalar_t d, ga_scalar_t u, const void *diag, void *ap,
+                                  void *pap, void *workspace, size_t workspace_bytes, void *stream) {
+  if (!valid_dtype(dt)) return fail(GA_ERR_INVALID_ARGUMENT, "cg_direction: bad dtype %d", (int)dt);
+  if (dt != GA_F32 && dt != GA_F64) return fail(GA_ERR_UNSUPPORTED, "cg_direction: F32 or F64 only");
+  if (n < 0) return fail(GA_ERR_INVALID_ARGUMENT, "cg_direction: n < 0");
+  if (!scalar_ok(beta.scale, dt) || !scalar_ok(l, dt) || !scalar_ok(d, dt) || !scalar_ok(u, dt))
+    return fail(GA_ERR_INVALID_ARGUMENT, "cg_direction: scalar dtype differs from array dtype");
+  if (!pap) return fail(GA_ERR_INVALID_ARGUMENT, "cg_direction: NULL pap");
+  if (n > 0 && (!r || !p_in || !p_out || !ap)) return fail(GA_ERR_INVALID_ARGUMENT, "cg_direction: NULL array");
+  const size_t bytes = (size_t)n * dtype_size(dt);
+  const void *ins[] = {r, p_in, diag};
+  for (const void *q : ins)
+    if (overlaps(p_out, q, bytes) || overlaps(ap, q, bytes))
+      return fail(GA_ERR_INVALID_ARGUMENT, "cg_direction: p_out / ap overlap an input (neighbours are read)");
+  if (overlaps(p_out, ap, bytes)) return fail(GA_ERR_INVALID_ARGUMENT, "cg_direction: p_out overlaps ap");
+  if (!workspace || workspace_bytes < gpuarray_reduce_workspace_bytes(dt, n))
+    return fail(GA_ERR_WORKSPACE, "cg_direction: workspace needs %zu bytes", gpuarray_reduce_workspace_bytes(dt, n));
+  return launch_cg_direction(dt, n, beta, r, p_in, p_out, l, d, u, diag, ap, pap, workspace, (cudaStream_t)stream);
+}
+
+ga_status_t gpuarray_cg_update(ga_dtype_t dt, int64_t n, ga_dscalar_t alpha, void *x, void *r, const void *p,
+                               const void *ap, void *rr, void *workspace, size_t workspace_bytes, void *stream) {
+  if (!valid_dtype(dt)) return fail(GA_ERR_INVALID_ARGUMENT, "cg_update: bad dtype %d", (int)dt);
+  if (dt != GA_F32 && dt != GA_F64) return fail(GA_ERR_UNSUPPORTED, "cg_update: F32 or F64 only");
+  if (n < 0) return fail(GA_ERR_INVALID_ARGUMENT, "cg_update: n < 0");
+  if (!scalar_ok(alpha.scale, dt)) return fail(GA_ERR_INVALID_ARGUMENT, "cg_update: scalar dtype differs");
+  if (!rr) return fail(GA_ERR_INVALID_ARGUMENT, "cg_update: NULL rr");
+  if (n > 0 && (!x || !r || !p || !ap)) return fail(GA_ERR_INVALID_ARGUMENT, "cg_update: NULL array");
+  const size_t bytes = (size_t)n * dtype_size(dt);
+  const void *all[] = {x, r, p, ap};
+  for (int i = 0; i < 4; ++i)
+    for (int j = i + 1; j < 4; ++j)
+      if (overlaps(all[i], all[j], bytes)) return fail(GA_ERR_INVALID_ARGUMENT, "cg_update: x, r, p, ap overlap");
+  if (!workspace || workspace_bytes < gpuarray_reduce_workspace_bytes(dt, n))
+    return fail(GA_ERR_WORKSPACE, "cg_update: workspace needs %zu bytes", gpuarray_reduce_workspace_bytes(dt, n));
+  return launch_cg_update(dt, n, alpha, x, r, p, ap, rr, workspace, (cudaStream_t)stream);
+}
+
 const char *gpuarray_status_string(ga_status_t s) {
   switch (s) {
     case GA_OK: return "GA_OK";

@@ -142,12 +142,52 @@ __device__ __forceinline__ T block_fold(T v, T *smem) {
   return v;
 }
 
+// Grid finish (§8(a) a4), called by every thread of every block with the
+// block's partial v (valid in thread 0): the partial goes to the workspace,
+// then __threadfence + an atomic ticket; the block drawing the last ticket
+// folds all partials in index order, resets the ticket (reusable by the next
+// call), runs the cross-GPU exchange if any, and writes *out.
+template <int OP, int BLOCK, typename Tacc>
+__device__ __forceinline__ void grid_finish(Tacc v, Tacc *smem, Tacc *partials, unsigned int *ticket, Tacc *out,
+                                            const Exchange &xg) {
+  __shared__ bool is_last;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = v;
+    __threadfence();
+    is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!is_last) return;
+
+  // Last block: fold the partials in index order (L2 reads, bypassing L1).
+  __threadfence();
+  // 8 independent L2 loads per thread in flight (a dependent one-by-one loop
+  // over up to 64 partials per thread cost several microseconds of tail).
+  Tacc w = Op<OP, Tacc>::neutral();
+  for (int base = threadIdx.x; base < (int)gridDim.x; base += BLOCK * 8) {
+    Tacc u[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = base + j * BLOCK;
+      u[j] = i < (int)gridDim.x ? ldcg<Tacc>(partials + i) : Op<OP, Tacc>::neutral();
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) w = Op<OP, Tacc>::fold(w, u[j]);
+  }
+  __syncthreads();  // smem reuse
+  w = block_fold<OP, BLOCK, Tacc>(w, smem);
+  if (threadIdx.x == 0) {
+    *ticket = 0u;
+    if (xg.world > 0) w = exchange_fold<OP, Tacc>(xg, w);
+    *out = w;
+  }
+}
+
 template <typename Tin, typename Tacc, int OP, int MAP, int UNROLL, int RED_BLOCK, int MINB>
 __global__ void __launch_bounds__(RED_BLOCK, MINB) reduce_kernel(RedArgs<Tin, Tacc> p) {
   constexpr int VEC = 32 / sizeof(Tin);
   constexpr bool HAS_Y = MAP == GA_MAP_MUL || MAP == GA_MAP_CONJ_MUL;
   __shared__ Tacc smem[RED_BLOCK / 32];
-  __shared__ bool is_last;
 
   const int64_t tid = (int64_t)blockIdx.x * RED_BLOCK + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * RED_BLOCK;
@@ -218,36 +258,7 @@ __global__ void __launch_bounds__(RED_BLOCK, MINB) reduce_kernel(RedArgs<Tin, Ta
   }
   Tacc v = block_fold<OP, RED_BLOCK, Tacc>(acc[0], smem);
 
-  if (threadIdx.x == 0) {
-    p.partials[blockIdx.x] = v;
-    __threadfence();
-    is_last = atomicAdd(p.ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!is_last) return;
-
-  // Last block: fold the partials in index order (L2 reads, bypassing L1).
-  __threadfence();
-  // 8 independent L2 loads per thread in flight (a dependent one-by-one loop
-  // over up to 64 partials per thread cost several microseconds of tail).
-  Tacc w = Op<OP, Tacc>::neutral();
-  for (int base = threadIdx.x; base < (int)gridDim.x; base += RED_BLOCK * 8) {
-    Tacc v[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int i = base + j * RED_BLOCK;
-      v[j] = i < (int)gridDim.x ? ldcg<Tacc>(p.partials + i) : Op<OP, Tacc>::neutral();
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) w = Op<OP, Tacc>::fold(w, v[j]);
-  }
-  __syncthreads();  // smem reuse
-  w = block_fold<OP, RED_BLOCK, Tacc>(w, smem);
-  if (threadIdx.x == 0) {
-    *p.ticket = 0u;  // reusable by the next call on this workspace
-    if (p.xg.world > 0) w = exchange_fold<OP, Tacc>(p.xg, w);
-    *p.out = w;
-  }
+  grid_finish<OP, RED_BLOCK, Tacc>(v, smem, p.partials, p.ticket, p.out, p.xg);
 }
 
 template <typename Tacc, int OP>

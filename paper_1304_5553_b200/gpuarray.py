@@ -159,6 +159,63 @@ def stencil3(l, d, u, x, diag=None, out=None):
     return out
 
 
+# --------------------------------------------------------------- fused CG steps (NEXT-4)
+def _dfactor(t, x, name):
+    if t is None:
+        return None
+    if t.numel() != 1 or t.dtype != x.dtype or t.device != x.device:
+        raise ValueError(f"{name} must be a 1-element tensor of x's dtype and device")
+    return t.data_ptr()
+
+
+def _scalar_out(out, x):
+    if out is None:
+        return torch.empty((), dtype=x.dtype, device=x.device)
+    if out.numel() != 1 or out.dtype != x.dtype or out.device != x.device:
+        raise ValueError("out must be a 1-element tensor of x's dtype on x's device")
+    return out
+
+
+def cg_direction(r, p_in, p_out, ap, beta=1.0, beta_num=None, beta_den=None, l=-1.0, d=2.0, u=-1.0, diag=None,
+                 out=None):
+    """One kernel: p_out = r + beta p_in, ap = A p_out (A = tridiag(l, d_i, u)),
+    returns p_out . ap as a 0-d device tensor.  beta is RN(beta *
+    RN(beta_num / beta_den)) with device factors (gpuarray_cg_direction)."""
+    _check_array("r", r)
+    for name, t in (("p_in", p_in), ("p_out", p_out), ("ap", ap)):
+        _same(r, t, name)
+    if diag is not None:
+        _same(r, diag, "diag")
+    out = _scalar_out(out, r)
+    dt = ga_dtype(r.dtype)
+    s = _stream(r)
+    nb = _abi.gpuarray_reduce_workspace_bytes(dt, r.numel())
+    w = workspace("reduce", r.device, s, nb)
+    check(_abi.gpuarray_cg_direction(dt, r.numel(), _abi.make_dscalar(dt, beta, _dfactor(beta_num, r, "beta_num"),
+                                                                      _dfactor(beta_den, r, "beta_den")),
+                                     _ptr(r), _ptr(p_in), _ptr(p_out), make_scalar(dt, l), make_scalar(dt, d),
+                                     make_scalar(dt, u), _ptr(diag) if diag is not None else None, _ptr(ap),
+                                     out.data_ptr(), w.data_ptr(), w.numel(), s))
+    return out
+
+
+def cg_update(x, r, p, ap, alpha=1.0, alpha_num=None, alpha_den=None, out=None):
+    """One kernel: x += alpha p, r -= alpha ap (in place), returns r . r of
+    the updated r as a 0-d device tensor (gpuarray_cg_update)."""
+    _check_array("x", x)
+    for name, t in (("r", r), ("p", p), ("ap", ap)):
+        _same(x, t, name)
+    out = _scalar_out(out, x)
+    dt = ga_dtype(x.dtype)
+    s = _stream(x)
+    nb = _abi.gpuarray_reduce_workspace_bytes(dt, x.numel())
+    w = workspace("reduce", x.device, s, nb)
+    check(_abi.gpuarray_cg_update(dt, x.numel(), _abi.make_dscalar(dt, alpha, _dfactor(alpha_num, x, "alpha_num"),
+                                                                   _dfactor(alpha_den, x, "alpha_den")),
+                                  _ptr(x), _ptr(r), _ptr(p), _ptr(ap), out.data_ptr(), w.data_ptr(), w.numel(), s))
+    return out
+
+
 # --------------------------------------------------------------- operators / cumath
 _BINARY = (_abi.GA_EW_MUL, _abi.GA_EW_DIV, _abi.GA_EW_MAX, _abi.GA_EW_MIN)
 

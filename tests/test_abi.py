@@ -24,7 +24,7 @@ def abi():
 
 def test_exports_every_declared_symbol(abi):
     declared = header_symbols()
-    assert len(declared) == 15
+    assert len(declared) == 17
     assert sorted(abi.EXPORTS) == declared
     for name in declared:
         assert hasattr(abi.LIB, name), name
@@ -38,7 +38,7 @@ def test_nm_shows_c_linkage(abi):
 
 
 def test_version_and_strings(abi):
-    assert abi.gpuarray_abi_version() == 3
+    assert abi.gpuarray_abi_version() == 4
     assert abi.gpuarray_status_string(abi.GA_OK) == "GA_OK"
     assert abi.gpuarray_status_string(abi.GA_ERR_CUDA) == "GA_ERR_CUDA"
     assert abi.gpuarray_status_string(99) == "GA_ERR_UNKNOWN"
@@ -95,6 +95,32 @@ def test_argument_validation_is_synchronous(abi):
     assert "in place" in abi.gpuarray_last_error()
     assert S(0, 0, I32, I32, 100, 4096, 8192, None, 0, 64, sw - 1, None) == abi.GA_ERR_WORKSPACE
     assert S(0, 0, I32, I32, 0, None, None, None, 0, None, 0, None) == abi.GA_OK           # n == 0 no-op
+
+
+def test_cg_step_validation(abi):
+    """The fused CG steps reject bad arguments before any launch."""
+    E = abi.GA_ERR_INVALID_ARGUMENT
+    F32 = abi.GA_F32
+    s32 = abi.make_scalar(F32, 1.0)
+    ds = abi.make_dscalar(F32, 1.0)
+    ws = abi.gpuarray_reduce_workspace_bytes(F32, 1000)
+    D = abi.gpuarray_cg_direction
+    # r=4096, p_in=8192, p_out=12288, ap=16384 (1000 floats = 4000 bytes each)
+    assert D(abi.GA_I32, 1000, abi.make_dscalar(abi.GA_I32, 1), 4096, 8192, 12288, s32, s32, s32, None, 16384, 64,
+             128, ws, None) == abi.GA_ERR_UNSUPPORTED
+    assert D(F32, 1000, ds, 4096, 8192, 8192, s32, s32, s32, None, 16384, 64, 128, ws, None) == E  # p_out = p_in
+    assert D(F32, 1000, ds, 4096, 8192, 12288, s32, s32, s32, None, 12290, 64, 128, ws, None) == E  # ap in p_out
+    assert D(F32, 1000, ds, 4096, 8192, 12288, s32, s32, s32, 16384, 16384, 64, 128, ws, None) == E  # ap = diag
+    assert D(F32, 1000, ds, 4096, 8192, 12288, s32, s32, s32, None, 16384, None, 128, ws, None) == E  # no pap
+    assert D(F32, 1000, ds, 4096, 8192, 12288, s32, s32, s32, None, 16384, 64, 128, ws - 1, None) == \
+        abi.GA_ERR_WORKSPACE
+    assert D(F32, 1000, abi.make_dscalar(abi.GA_F64, 1.0), 4096, 8192, 12288, s32, s32, s32, None, 16384, 64, 128,
+             ws, None) == E                                                                     # scalar dtype
+    U = abi.gpuarray_cg_update
+    assert U(F32, 1000, ds, 4096, 4096, 8192, 12288, 64, 128, ws, None) == E                   # x = r
+    assert U(F32, 1000, ds, 4096, 8192, 12288, 12300, 64, 128, ws, None) == E                  # p, ap overlap
+    assert U(F32, -1, ds, 4096, 8192, 12288, 16384, 64, 128, ws, None) == E
+    assert U(abi.GA_C64, 10, ds, 4096, 8192, 12288, 16384, 64, 128, ws, None) == abi.GA_ERR_UNSUPPORTED
 
 
 def test_python_error_mapping(abi):

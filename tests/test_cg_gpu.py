@@ -132,3 +132,114 @@ def test_cg_graph_converges_poisson():
     assert res.converged and res.iterations <= 72
     A = 2 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)
     assert np.allclose(res.x.cpu().numpy(), np.linalg.solve(A, np.ones(n)), rtol=1e-8, atol=0)
+
+
+# ------------------------------------------------------------------ fused CG steps (R28)
+def _sdata(dt, n, seed, unit=False):
+    if dt == np.float32:
+        return synth.host_fill(synth.F32_U01 if unit else synth.F32_S11, seed, n)
+    return synth.host_fill(synth.F64_U01 if unit else synth.F64_S11, seed, n)
+
+
+def _dot_tol(dt, n, ref, sumabs):
+    u = 2.0 ** -24 if dt == np.float32 else 2.0 ** -53
+    rel = 1e-5 if dt == np.float32 else 1e-13
+    return max(rel * abs(ref), n * u * sumabs)
+
+
+FUSED_SIZES = [1, 2, 7, 8, 9, 255, 4099, 100_003, 1_000_003, (1 << 20) + 17]
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("n", FUSED_SIZES)
+@pytest.mark.parametrize("with_diag", [False, True])
+def test_cg_direction_matches_composition(dt, n, with_diag):
+    """p_out, ap bit-exact against the oracle's axpbyz(1, r, beta, p_in) then
+    stencil3; p_out . ap within the dot tolerance (R9/R10); beta formed from
+    device factors exactly as ga_dscalar_t says (RN(scale * RN(num / den)))."""
+    tdt = NPT[dt]
+    r, pin = _sdata(dt, n, 11), _sdata(dt, n, 12)
+    diag = (dt(3.0) + _sdata(dt, n, 13, unit=True)).astype(dt) if with_diag else None
+    l, d, u = dt(-1.25), dt(2.5), dt(-0.75)
+    num = torch.tensor([0.37], dtype=tdt, device=DEV)
+    den = torch.tensor([-1.9], dtype=tdt, device=DEV)
+    beta = dt(dt(2.0) * dt(dt(0.37) / dt(-1.9)))
+    p_ref = oracle.axpbyz(dt(1), r, beta, pin)
+    ap_ref = oracle.stencil3(l, d, u, p_ref, diag=diag)
+    dot_ref, sa = oracle.reduce(oracle.SUM, oracle.MAP_MUL, p_ref, ap_ref, return_sumabs=True)
+    for offs in (0, 3):  # vector path, scalar path
+        pout = to_dev(np.zeros(n, dt), offs)
+        ap = to_dev(np.zeros(n, dt), offs)
+        got = G.cg_direction(to_dev(r, offs), to_dev(pin, offs), pout, ap, beta=2.0, beta_num=num, beta_den=den,
+                             l=float(l), d=float(d), u=float(u), diag=to_dev(diag, offs) if with_diag else None)
+        assert np.array_equal(bits(pout.cpu().numpy()), bits(p_ref))
+        assert np.array_equal(bits(ap.cpu().numpy()), bits(ap_ref))
+        assert abs(float(got.item()) - dot_ref) <= _dot_tol(dt, n, dot_ref, sa)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("n", FUSED_SIZES)
+def test_cg_update_matches_composition(dt, n):
+    """x' = axpbyz(1, x, alpha, p), r' = axpbyz(1, r, -alpha, ap) bit-exact;
+    r'.r' within tolerance; alpha = RN(1 * RN(num / den))."""
+    tdt = NPT[dt]
+    x, r, p, ap = _sdata(dt, n, 21), _sdata(dt, n, 22), _sdata(dt, n, 23), _sdata(dt, n, 24)
+    num = torch.tensor([1.7], dtype=tdt, device=DEV)
+    den = torch.tensor([3.1], dtype=tdt, device=DEV)
+    alpha = dt(dt(1.7) / dt(3.1))
+    x_ref = oracle.axpbyz(dt(1), x, alpha, p)
+    r_ref = oracle.axpbyz(dt(1), r, -alpha, ap)
+    rr_ref, sa = oracle.reduce(oracle.SUM, oracle.MAP_SQUARE, r_ref, return_sumabs=True)
+    for offs in (0, 1):
+        xd, rd = to_dev(x, offs), to_dev(r, offs)
+        got = G.cg_update(xd, rd, to_dev(p, offs), to_dev(ap, offs), alpha=1.0, alpha_num=num, alpha_den=den)
+        assert np.array_equal(bits(xd.cpu().numpy()), bits(x_ref))
+        assert np.array_equal(bits(rd.cpu().numpy()), bits(r_ref))
+        assert abs(float(got.item()) - rr_ref) <= _dot_tol(dt, n, rr_ref, sa)
+
+
+def test_cg_fused_edge_cases():
+    """n == 0 writes 0; a zero numerator gives a zero factor even over 0
+    (a converged iteration stays finite); overlapping outputs are rejected."""
+    for dt in (torch.float32, torch.float64):
+        e = torch.empty(0, dtype=dt, device=DEV)
+        assert float(G.cg_direction(e, e, e, e).item()) == 0.0
+        assert float(G.cg_update(e, e, e, e).item()) == 0.0
+        n = 1000
+        z = torch.zeros(1, dtype=dt, device=DEV)
+        r, pin = torch.zeros(n, dtype=dt, device=DEV), torch.full((n,), 7.0, dtype=dt, device=DEV)
+        pout, ap = torch.empty_like(r), torch.empty_like(r)
+        pap = G.cg_direction(r, pin, pout, ap, beta_num=z, beta_den=z)
+        assert float(pap.item()) == 0.0 and bool((pout == 0).all()) and bool((ap == 0).all())
+        x = torch.ones(n, dtype=dt, device=DEV)
+        rr = G.cg_update(x, r, pout, ap, alpha_num=z, alpha_den=pap)
+        assert float(rr.item()) == 0.0 and bool((x == 1).all())
+        with pytest.raises(ValueError):
+            G.cg_direction(r, pin, pin, ap)        # p_out aliases p_in
+        with pytest.raises(ValueError):
+            G.cg_update(x, x, pout, ap)            # x aliases r
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+@pytest.mark.parametrize("with_diag", [False, True])
+def test_cg_graph_fused_vs_unfused(dt, with_diag):
+    """The fused iteration (2 kernels) and the 6-kernel one converge on the
+    same diagonally dominant system to the same tolerance, in about the same
+    number of iterations; the fused solution's residual, recomputed by the
+    oracle, meets rtol."""
+    n = (1 << 20) + 5
+    npdt = np.float32 if dt == torch.float32 else np.float64
+    bh = _sdata(npdt, n, 5)
+    dh = (4.0 + synth.host_fill(synth.F64_U01, 6, n)).astype(npdt) if with_diag else None
+    b = torch.from_numpy(bh).to(DEV)
+    dd = torch.from_numpy(dh).to(DEV) if with_diag else None
+    rtol = 1e-5 if dt == torch.float32 else 1e-12
+    fused = gcg.cg_graph(b, offdiag=-1.0, d=4.0, diag=dd, rtol=rtol, maxiter=200, block=8, fused=True)
+    plain = gcg.cg_graph(b, offdiag=-1.0, d=4.0, diag=dd, rtol=rtol, maxiter=200, block=8, fused=False)
+    assert fused.converged and plain.converged
+    assert abs(fused.iterations - plain.iterations) <= 8
+    x = fused.x.cpu().numpy().astype(np.float64)
+    r = bh.astype(np.float64) - oracle.stencil3(-1.0, 4.0, -1.0, x, diag=None if dh is None else dh.astype(np.float64))
+    u = 2.0 ** -24 if dt == torch.float32 else 2.0 ** -53
+    bn = np.linalg.norm(bh.astype(np.float64))
+    assert np.linalg.norm(r) <= rtol * bn + 50 * u * bn
