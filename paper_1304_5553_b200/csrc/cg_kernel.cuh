@@ -1,0 +1,206 @@
+// cg_kernel.cuh — the fused CG iteration kernels (see cg.cu for what they
+// compute and why), templated on the per-thread unroll and the minimum CTAs
+// per SM so cg.cu instantiates the tuned shape and tools/lab/cg_lab.cu can
+// time others.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ga_device.cuh"
+#include "ga_host.h"
+#include "reduce_kernel.cuh"
+
+namespace ga {
+namespace cg_detail {
+
+using namespace red_detail;
+
+constexpr int CG_BLOCK = 256;
+
+template <typename T>
+struct DirArgs {
+  int64_t n, nvec;            // nvec = 0: scalar path for everything
+  T bscale;                   // beta = RN(bscale * RN(*bnum / *bden))
+  const T *bnum, *bden;
+  T l, d, u;                  // operator tridiag(l, d_i, u)
+  const T *diag;              // nullptr: constant d
+  const T *r, *pin;
+  T *pout, *ap;
+  T *out, *partials;
+  unsigned int *ticket;
+};
+
+template <typename T>
+struct UpdArgs {
+  int64_t n, nvec;
+  T ascale;                   // alpha = RN(ascale * RN(*anum / *aden))
+  const T *anum, *aden;
+  T *x, *r;
+  const T *p, *ap;
+  T *out, *partials;
+  unsigned int *ticket;
+};
+
+// p' = RN(RN(1*r) + RN(beta*p)) — gpuarray_axpbyz(1, r, beta, p) (R1).
+template <typename T>
+__device__ __forceinline__ T dir_p(T beta, T r, T p) {
+  return e_add(e_mul(T(1), r), e_mul(beta, p));
+}
+template <typename T>
+__device__ __forceinline__ T pnew_at(const DirArgs<T> &a, T beta, int64_t j) {
+  return (j >= 0 && j < a.n) ? dir_p(beta, a.r[j], a.pin[j]) : T(0);
+}
+// (A p')_i with gpuarray_stencil3's operation order (R25).
+template <typename T>
+__device__ __forceinline__ T point(const DirArgs<T> &a, int64_t i, T pm, T p0, T pp, T di) {
+  T acc = e_mul(di, p0);
+  if (i > 0) acc = e_add(e_mul(a.l, pm), acc);
+  if (i + 1 < a.n) acc = e_add(acc, e_mul(a.u, pp));
+  return acc;
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ T lane_tree(T (&acc)[VEC]) {
+#pragma unroll
+  for (int w = VEC / 2; w >= 1; w >>= 1) {
+#pragma unroll
+    for (int k = 0; k < w; ++k) acc[k] = e_add(acc[k], acc[k + w]);
+  }
+  return acc[0];
+}
+
+// DIAG: a diagonal array is read (a.diag != nullptr) instead of the constant d.
+template <typename T, int CG_UNROLL, int CG_MINB, bool DIAG>
+__global__ void __launch_bounds__(CG_BLOCK, CG_MINB) cg_direction_kernel(DirArgs<T> a) {
+  constexpr int VEC = 32 / sizeof(T);
+  __shared__ T smem[CG_BLOCK / 32];
+  const int lane = threadIdx.x & 31;
+  const T beta = coef(a.bscale, a.bnum, a.bden);
+  T acc[VEC];
+#pragma unroll
+  for (int k = 0; k < VEC; ++k) acc[k] = T(0);
+
+  // scalar part: everything after the last whole vector (or all of it)
+  const int64_t tid = (int64_t)blockIdx.x * CG_BLOCK + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * CG_BLOCK;
+  for (int64_t i = a.nvec * VEC + tid; i < a.n; i += nthreads) {
+    const T p0 = pnew_at(a, beta, i);
+    const T y = point(a, i, pnew_at(a, beta, i - 1), p0, pnew_at(a, beta, i + 1), DIAG ? a.diag[i] : a.d);
+    a.pout[i] = p0;
+    a.ap[i] = y;
+    acc[VEC - 1] = e_fma(p0, y, acc[VEC - 1]);
+  }
+
+  constexpr int64_t CHUNK = (int64_t)CG_BLOCK * CG_UNROLL;
+  for (int64_t base = (int64_t)blockIdx.x * CHUNK + threadIdx.x; base - threadIdx.x < a.nvec;
+       base += (int64_t)gridDim.x * CHUNK) {
+    V32 rv[CG_UNROLL], pv[CG_UNROLL], dv[DIAG ? CG_UNROLL : 1];
+    T hl[CG_UNROLL], hr[CG_UNROLL];  // halo p' (lane 0: left, lane 31 / last vector: right)
+#pragma unroll
+    for (int j = 0; j < CG_UNROLL; ++j) {
+      const int64_t v = base + j * CG_BLOCK;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) rv[j].r[k] = pv[j].r[k] = 0;
+      hl[j] = hr[j] = T(0);
+      if (v < a.nvec) {
+        rv[j] = ld_nc_256(a.r + v * VEC);
+        pv[j] = ld_nc_256(a.pin + v * VEC);
+        if constexpr (DIAG) dv[j] = ld_nc_256(a.diag + v * VEC);
+        if (lane == 0) hl[j] = pnew_at(a, beta, v * VEC - 1);
+        if (lane == 31 || v + 1 >= a.nvec) hr[j] = pnew_at(a, beta, v * VEC + VEC);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CG_UNROLL; ++j) {
+      const int64_t v = base + j * CG_BLOCK;
+      T pn[VEC];
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) pn[k] = dir_p(beta, vget<T>(rv[j], k), vget<T>(pv[j], k));
+      T left = __shfl_up_sync(0xffffffffu, pn[VEC - 1], 1);
+      T right = __shfl_down_sync(0xffffffffu, pn[0], 1);
+      if (v < a.nvec) {
+        if (lane == 0) left = hl[j];
+        if (lane == 31 || v + 1 >= a.nvec) right = hr[j];
+        const int64_t i0 = v * VEC;
+        const bool interior = i0 > 0 && i0 + VEC < a.n;  // every element has both neighbours
+        V32 po, yo;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+          T di = a.d;
+          if constexpr (DIAG) di = vget<T>(dv[DIAG ? j : 0], k);
+          const T pm = k == 0 ? left : pn[k - 1], pp = k == VEC - 1 ? right : pn[k + 1];
+          const T y = interior ? e_add(e_add(e_mul(a.l, pm), e_mul(di, pn[k])), e_mul(a.u, pp))
+                               : point(a, i0 + k, pm, pn[k], pp, di);
+          vset<T>(po, k, pn[k]);
+          vset<T>(yo, k, y);
+          acc[k] = e_fma(pn[k], y, acc[k]);
+        }
+        st_256(a.pout + i0, po);
+        st_256(a.ap + i0, yo);
+      }
+    }
+  }
+  const T v = block_fold<GA_OP_SUM, CG_BLOCK, T>(lane_tree<T, VEC>(acc), smem);
+  grid_finish<GA_OP_SUM, CG_BLOCK, T>(v, smem, a.partials, a.ticket, a.out, Exchange{});
+}
+
+template <typename T, int CG_UNROLL, int CG_MINB>
+__global__ void __launch_bounds__(CG_BLOCK, CG_MINB) cg_update_kernel(UpdArgs<T> a) {
+  constexpr int VEC = 32 / sizeof(T);
+  __shared__ T smem[CG_BLOCK / 32];
+  // x' = RN(RN(1*x) + RN(alpha*p)), r' = RN(RN(1*r) + RN(-alpha*ap)):
+  // gpuarray_axpbyz_ds(1, x, alpha, p) and (1, r, -alpha, ap), whose b
+  // factors are RN(+-ascale * q) = +-alpha exactly.
+  const T alpha = coef(a.ascale, a.anum, a.aden);
+  const T nalpha = coef(-a.ascale, a.anum, a.aden);
+  T acc[VEC];
+#pragma unroll
+  for (int k = 0; k < VEC; ++k) acc[k] = T(0);
+
+  const int64_t tid = (int64_t)blockIdx.x * CG_BLOCK + threadIdx.x;
+  const int64_t nthreads = (int64_t)gridDim.x * CG_BLOCK;
+  for (int64_t i = a.nvec * VEC + tid; i < a.n; i += nthreads) {
+    a.x[i] = e_add(e_mul(T(1), a.x[i]), e_mul(alpha, a.p[i]));
+    const T rn = e_add(e_mul(T(1), a.r[i]), e_mul(nalpha, a.ap[i]));
+    a.r[i] = rn;
+    acc[VEC - 1] = e_fma(rn, rn, acc[VEC - 1]);
+  }
+
+  constexpr int64_t CHUNK = (int64_t)CG_BLOCK * CG_UNROLL;
+  for (int64_t base = (int64_t)blockIdx.x * CHUNK + threadIdx.x; base - threadIdx.x < a.nvec;
+       base += (int64_t)gridDim.x * CHUNK) {
+    V32 xv[CG_UNROLL], pv[CG_UNROLL], rv[CG_UNROLL], av[CG_UNROLL];
+#pragma unroll
+    for (int j = 0; j < CG_UNROLL; ++j) {
+      const int64_t v = base + j * CG_BLOCK;
+      if (v < a.nvec) {
+        // x and r are rewritten in place: coherent loads
+        xv[j] = ld_256(a.x + v * VEC);
+        rv[j] = ld_256(a.r + v * VEC);
+        pv[j] = ld_nc_256(a.p + v * VEC);
+        av[j] = ld_nc_256(a.ap + v * VEC);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CG_UNROLL; ++j) {
+      const int64_t v = base + j * CG_BLOCK;
+      if (v < a.nvec) {
+        V32 xo, ro;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+          vset<T>(xo, k, e_add(e_mul(T(1), vget<T>(xv[j], k)), e_mul(alpha, vget<T>(pv[j], k))));
+          const T rn = e_add(e_mul(T(1), vget<T>(rv[j], k)), e_mul(nalpha, vget<T>(av[j], k)));
+          vset<T>(ro, k, rn);
+          acc[k] = e_fma(rn, rn, acc[k]);
+        }
+        st_256(a.x + v * VEC, xo);
+        st_256(a.r + v * VEC, ro);
+      }
+    }
+  }
+  const T v = block_fold<GA_OP_SUM, CG_BLOCK, T>(lane_tree<T, VEC>(acc), smem);
+  grid_finish<GA_OP_SUM, CG_BLOCK, T>(v, smem, a.partials, a.ticket, a.out, Exchange{});
+}
+
+}  // namespace cg_detail
+}  // namespace ga

@@ -113,16 +113,21 @@ def test_axpbyz_ds_bit_exact():
 
 
 def test_cg_graph_matches_host_cg_f64():
-    """float64: the device-scalar iteration computes the same alpha/beta bits
-    as the host one (RN(rs/pAp) either way), so x and the residuals agree
-    exactly over the same number of iterations."""
+    """float64: the unfused device-scalar iteration runs the same kernels as
+    the host one and forms the same alpha/beta bits (RN(rs/pAp) either way),
+    so x and the residuals agree exactly over the same number of iterations.
+    The fused iteration reduces p.Ap and r.r in another order (R28): close,
+    not identical."""
     n = 1 << 16
     b = torch.from_numpy(synth.host_fill(synth.F64_S11, 7, n)).to(DEV)
     ref = gcg.cg(b, offdiag=-1.0, d=4.0, rtol=0.0, maxiter=32)
-    got = gcg.cg_graph(b, offdiag=-1.0, d=4.0, rtol=0.0, maxiter=32, block=16)
+    got = gcg.cg_graph(b, offdiag=-1.0, d=4.0, rtol=0.0, maxiter=32, block=16, fused=False)
     assert got.iterations == ref.iterations == 32
     assert torch.equal(got.x, ref.x)
     assert got.residual_norms[-1] == ref.residual_norms[-1]
+    fused = gcg.cg_graph(b, offdiag=-1.0, d=4.0, rtol=0.0, maxiter=32, block=16, fused=True)
+    assert fused.iterations == 32
+    assert torch.allclose(fused.x, ref.x, rtol=1e-9, atol=1e-12)
 
 
 def test_cg_graph_converges_poisson():
