@@ -73,6 +73,20 @@ def test_axpbyz_bit_exact(dt, n):
 
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_axpbyz_unfused_composition_equals_fused(dt):
+    """The temporaries evaluation t = a*x; u = b*y; z = t + u (axpbz with
+    b = -0.0, then axpbyz with unit coefficients; tools/fusion_bench.py) is
+    bit-identical to the single pass (R1: RN(RN(a x) + RN(b y)))."""
+    n = 1_000_003
+    x, y = host_data(dt, n, 1, signed=True), host_data(dt, n, 2, signed=True)
+    xd, yd = to_dev(x), to_dev(y)
+    t = G.axpbz(5.0, xd, -0.0)
+    u = G.axpbz(-6.0, yd, -0.0)
+    z = G.axpbyz(1.0, t, 1.0, u).cpu().numpy()
+    assert_bit_exact(z, oracle.axpbyz(dt(5.0), x, dt(-6.0), y))
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
 @pytest.mark.parametrize("offs", [(1, 1, 1), (3, 3, 3), (7, 7, 7), (1, 2, 3), (0, 5, 0), (2, 0, 0)])
 def test_axpbyz_unaligned_views(dt, offs):
     n = 10007
