@@ -322,8 +322,10 @@ __device__ __forceinline__ void draw_tile(const A &p, uint32_t &tile, uint32_t &
 //   phase 3  every warp re-reads its slice (now L2-resident, evict_first),
 //            scans it row by row and stores (STG.128, 512 B per warp).
 // ===========================================================================
+// P1U: rows in flight per warp in phase 1 (its only live state is the raw
+// rows, so it can exceed phase 3's UNROLL).
 template <int OP, typename T, typename Tin, int WARPS, int ROWS, int UNROLL, int DEPTH, bool NC, bool EXCLUSIVE,
-          bool EARLY>
+          bool EARLY, int P1U = UNROLL>
 __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p) {
   using O = Op<OP, T>;
   constexpr int E = Chunk<Tin>::E;  // elements per lane per row
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p)
   constexpr bool WIDEN = sizeof(T) != sizeof(Tin);
   static_assert(!WIDEN || (sizeof(T) == 8 && sizeof(Tin) == 4), "widening is 4 -> 8 bytes");
   constexpr int64_t TILE = (int64_t)WARPS * ROWS * ROW;
-  static_assert(ROWS % UNROLL == 0, "ROWS must be a multiple of UNROLL");
+  static_assert(ROWS % UNROLL == 0 && ROWS % P1U == 0, "ROWS must be a multiple of UNROLL and P1U");
   static_assert(WARPS <= 32, "slice folds are scanned by one warp");
   __shared__ uint32_t s_tile, s_epoch;
   __shared__ T s_slice[WARPS];
@@ -373,12 +375,12 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p)
   // phase 1: slice folds
   T acc = neutral;
 #pragma unroll 1
-  for (int r0 = 0; r0 < ROWS; r0 += UNROLL) {
-    uint4 raw[UNROLL];
+  for (int r0 = 0; r0 < ROWS; r0 += P1U) {
+    uint4 raw[P1U];
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) raw[u] = load_raw(r0 + u, keep);
+    for (int u = 0; u < P1U; ++u) raw[u] = load_raw(r0 + u, keep);
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
+    for (int u = 0; u < P1U; ++u) {
       T v[E];
       widen(raw[u], v);
 #pragma unroll

@@ -7,43 +7,30 @@
 
 using namespace ga::scan_detail;
 
-template <typename T, int W, int R, int U, int D>
+template <typename T, int W, int R, int U, int D, int P1U = U>
 static int run(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   constexpr int64_t TILE = (int64_t)W * R * 512 / sizeof(T);
   ScanArgs<T> p = make_args<T>(n, TILE, in, out, nullptr, 0, ws);
-  scan_l2_kernel<GA_OP_SUM, T, T, W, R, U, D, true, true, true><<<(int)p.num_tiles, W * 32, 0, s>>>(p);
+  scan_l2_kernel<GA_OP_SUM, T, T, W, R, U, D, true, true, true, P1U><<<(int)p.num_tiles, W * 32, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : 100 + (int)e;
 }
 
-#define V(X)                  \
-  X(0, int32_t, 24, 32, 8, 8) \
-  X(1, int32_t, 24, 16, 8, 8) \
-  X(2, int32_t, 24, 8, 8, 8)  \
-  X(3, int32_t, 16, 8, 8, 8)  \
-  X(4, int32_t, 8, 8, 8, 8)   \
-  X(5, int32_t, 8, 16, 8, 8)  \
-  X(6, int32_t, 12, 8, 8, 8)  \
-  X(7, int32_t, 32, 8, 8, 8)  \
-  X(8, int32_t, 4, 8, 8, 8)   \
-  X(9, int32_t, 8, 4, 4, 8)   \
-  X(10, int32_t, 16, 4, 4, 8) \
-  X(11, int32_t, 32, 4, 4, 8) \
-  X(12, int32_t, 24, 24, 8, 8) \
-  X(20, int64_t, 24, 32, 8, 4) \
-  X(21, int64_t, 24, 8, 8, 4)  \
-  X(22, int64_t, 8, 8, 8, 4)   \
-  X(23, int64_t, 16, 8, 8, 4)  \
-  X(24, int64_t, 8, 4, 4, 4)   \
-  X(25, int64_t, 32, 8, 8, 4)  \
-  X(26, int64_t, 24, 16, 8, 4) \
-  X(27, int64_t, 32, 16, 8, 4) \
-  X(28, int64_t, 16, 16, 8, 4)
+#define V(X)                        \
+  X(0, int32_t, 24, 32, 8, 8, 8)    \
+  X(1, int32_t, 24, 32, 8, 8, 16)   \
+  X(2, int32_t, 24, 32, 8, 8, 32)   \
+  X(3, int32_t, 24, 32, 4, 8, 16)   \
+  X(4, int32_t, 16, 32, 8, 8, 16)   \
+  X(5, int32_t, 32, 16, 8, 8, 16)   \
+  X(6, int32_t, 24, 64, 8, 8, 16)   \
+  X(20, int64_t, 24, 32, 8, 4, 8)   \
+  X(21, int64_t, 24, 32, 8, 4, 16)
 
 extern "C" int lab_scan(int v, int64_t n, const void *in, void *out, void *ws, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
   switch (v) {
-#define C(id, T, W, R, U, D) case id: return run<T, W, R, U, D>(n, in, out, ws, s);
+#define C(id, T, W, R, U, D, P) case id: return run<T, W, R, U, D, P>(n, in, out, ws, s);
     V(C)
 #undef C
   }
@@ -51,7 +38,7 @@ extern "C" int lab_scan(int v, int64_t n, const void *in, void *out, void *ws, v
 }
 extern "C" int64_t lab_scan_tile(int v) {
   switch (v) {
-#define C(id, T, W, R, U, D) case id: return (int64_t)W * R * 512 / sizeof(T);
+#define C(id, T, W, R, U, D, P) case id: return (int64_t)W * R * 512 / sizeof(T);
     V(C)
 #undef C
   }

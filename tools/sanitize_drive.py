@@ -1,0 +1,64 @@
+"""Exercise every libgpuarray kernel family at small, ragged and unaligned
+sizes (no checks: the parity tests do that) so compute-sanitizer can watch
+for out-of-bounds accesses, races and barrier misuse:
+
+    compute-sanitizer --tool memcheck|racecheck|synccheck python tools/sanitize_drive.py"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_1304_5553_b200 import gpuarray as G  # noqa: E402
+
+dev = torch.device("cuda:0")
+
+
+def arr(n, dt, off=0):
+    buf = (torch.rand(n + off, device=dev) * 10).to(dt)
+    return buf[off:]
+
+
+for n in (1, 7, 33, 1000, 4099, 70_001, 300_007):
+    for off in (0, 1):
+        for dt in (torch.float32, torch.float64, torch.int32, torch.int64):
+            x, y = arr(n, dt, off), arr(n, dt, off)
+            G.axpbyz(2, x, 3, y)
+            G.axpbz(2, x, 1)
+            G.sum(x)
+            G.max(x)
+            G.min(x)
+            G.dot(x, y)
+            G.norm2sq(x)
+            G.elementwise(G._abi.GA_EW_MUL, x, y)
+            G.elementwise(G._abi.GA_EW_MAX, x, y)
+            G.elementwise(G._abi.GA_EW_NEG, x)
+            for op in (G.SUM, G.MAX, G.MIN):
+                G.scan(x, op=op)
+                G.scan(x, exclusive=True, op=op, carry=arr(2, dt))
+            if dt == torch.int32:
+                G.scan(x, out_dtype=torch.int64)
+            if dt == torch.float32:
+                G.scan(x, out_dtype=torch.float64, exclusive=True)
+            if dt.is_floating_point:
+                G.elementwise(G._abi.GA_EW_SQRT, x)
+                G.elementwise(G._abi.GA_EW_EXP, x)
+                G.stencil3(-1, 2, -1, x)
+                G.stencil3(-1, 2, -1, x, diag=arr(n, dt, off))
+                one = torch.ones(1, dtype=dt, device=dev)
+                G.axpbyz_ds(1.0, x, 1.0, y, b_num=one, b_den=one)
+                p2, ap = arr(n, dt, off), arr(n, dt, off)
+                G.cg_direction(x, y, p2, ap, beta_num=one, beta_den=one)
+                G.cg_direction(x, y, p2, ap, beta_num=one, beta_den=one, diag=arr(n, dt, off))
+                G.cg_update(arr(n, dt, off), arr(n, dt, off), p2, ap, alpha_num=one, alpha_den=one)
+        for cdt in (torch.complex64, torch.complex128):
+            xc = torch.randn(n + off, dtype=cdt, device=dev)[off:]
+            yc = torch.randn(n + off, dtype=cdt, device=dev)[off:]
+            G.axpbyz(1 + 2j, xc, 3, yc)
+            G.vdot(xc, yc)
+            G.dot(xc, yc)
+            G.norm2sq(xc)
+    torch.cuda.synchronize()
+print("drive ok", G.launch_count(), "launches")
