@@ -120,7 +120,7 @@ def test_c3_int_sum_max_scan_2p30(dt):
     _check_scan_windows(out, n, kind, 3, 0, 9, npdt, exclusive=False)
 
 
-def _check_scan_windows(out, n, kind, seed, lo, hi, npdt, exclusive, window=1 << 16):
+def _check_scan_windows(out, n, kind, seed, lo, hi, npdt, exclusive, window=1 << 16, widen=False):
     chunk = bigcheck.CHUNK
     sums = bigcheck.chunk_sums_int(n, kind, seed, lo, hi, chunk)
     w = 1 << (np.dtype(npdt).itemsize * 8)
@@ -131,7 +131,8 @@ def _check_scan_windows(out, n, kind, seed, lo, hi, npdt, exclusive, window=1 <<
         m = min(window, n - start)
         xin = synth.host_fill(kind, seed, m, start=start, lo=lo, hi=hi)
         carry = npdt(((prefix + w // 2) % w) - w // 2)
-        ref = oracle.scan(oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE, xin, carry=carry)
+        ref = oracle.scan(oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE, xin, carry=carry,
+                          out_dtype=npdt if widen else None)
         got = out[start:start + m].cpu().numpy()
         assert np.array_equal(got, ref), f"window at {start}"
         checked += m
@@ -144,6 +145,19 @@ def _check_scan_windows(out, n, kind, seed, lo, hi, npdt, exclusive, window=1 <<
     expect = (expect + w // 2) % w - w // 2
     assert last == expect
     assert checked >= min(n, len(sums) * window)
+
+
+def test_c3_widening_scan_2p30():
+    """int32 -> int64 inclusive scan at C3's size (NEXT-2, R27): the U{0..9}
+    prefix sums reach ~4.8e9, past int32's range, and must not wrap."""
+    n = 1 << 30
+    need_bytes(12 * n)
+    k = synth.device_fill(synth.I32_RANGE, 3, n, lo=0, hi=9, device=DEV)
+    out = G.scan(k, out_dtype=torch.int64)
+    del k
+    free()
+    assert int(out[-1].item()) > (1 << 31)
+    _check_scan_windows(out, n, synth.I32_RANGE, 3, 0, 9, np.int64, exclusive=False, widen=True)
 
 
 def test_c4_dot_norm2_2p33():
