@@ -30,9 +30,9 @@ static int run(int64_t n, const float *x, const float *y, float *out, void *ws, 
 #define V(X) \
   X(0, GA_MAP_ID, 4, 512, 1) X(1, GA_MAP_ID, 4, 512, 2) X(2, GA_MAP_ID, 4, 512, 3) X(3, GA_MAP_ID, 4, 256, 4) \
   X(4, GA_MAP_ID, 4, 256, 6) X(5, GA_MAP_ID, 8, 256, 4) X(6, GA_MAP_ID, 2, 512, 3) X(7, GA_MAP_ID, 4, 1024, 1) \
-  X(8, GA_MAP_ID, 2, 256, 8) \
+  X(8, GA_MAP_ID, 2, 256, 8) X(9, GA_MAP_ID, 1, 256, 8) \
   X(10, GA_MAP_MUL, 2, 512, 1) X(11, GA_MAP_MUL, 2, 512, 2) X(12, GA_MAP_MUL, 2, 512, 3) X(13, GA_MAP_MUL, 2, 256, 4) \
-  X(14, GA_MAP_MUL, 2, 256, 6) X(15, GA_MAP_MUL, 4, 256, 4) X(16, GA_MAP_MUL, 1, 512, 4) X(17, GA_MAP_MUL, 2, 1024, 1)
+  X(14, GA_MAP_MUL, 2, 256, 6) X(15, GA_MAP_MUL, 4, 256, 4) X(16, GA_MAP_MUL, 1, 512, 4) X(17, GA_MAP_MUL, 2, 1024, 1) X(18, GA_MAP_MUL, 1, 256, 8)
 
 extern "C" int red_lab(int v, int64_t n, const float *x, const float *y, float *out, void *ws, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
