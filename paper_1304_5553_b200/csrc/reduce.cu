@@ -15,10 +15,13 @@
 //      tools/lab/red_lab.cu; the CTA shape is from red_shape_lab.cu);
 //   2. fixed-order lane tree -> warp xor-butterfly -> per-warp partial in
 //      shared memory -> warp 0 folds the block partial;
-//   3. last-block-done finish: the block partial goes to workspace, then
-//      __threadfence + an atomic ticket; the block that draws the last ticket
-//      folds all partials in index order, writes *out and resets the ticket
-//      (no second launch, no host sync, no memset between calls).
+//   3. last-block-done finish, two levels: the block partial goes to
+//      workspace, then __threadfence + its group's atomic ticket (groups of
+//      128 consecutive blocks); the block that draws a group's last ticket
+//      folds the group in index order and takes the global ticket; the block
+//      that draws the last one folds the group partials in order, writes
+//      *out and resets the tickets (no second launch, no host sync, no
+//      memset between calls).
 // Deterministic for a given n (the grid depends on n only, not on the
 // device): every fold order above is fixed.
 #include <cuda_runtime.h>
@@ -119,7 +122,7 @@ ga_status_t maxmin(ga_map_t map, int64_t n, const void *x, const void *y, void *
 
 }  // namespace
 
-size_t reduce_workspace_bytes() { return RED_HEADER + (size_t)RED_MAX_PARTIALS * 16; }  // up to c128 partials
+size_t reduce_workspace_bytes() { return RED_WS_BYTES; }  // up to c128 partials
 
 ga_status_t launch_reduce(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
                           const void *x, const void *y, void *out, void *ws, const Exchange &xg, cudaStream_t s) {

@@ -15,7 +15,15 @@ namespace red_detail {
 
 
 constexpr int RED_MAX_PARTIALS = 32768;
-constexpr size_t RED_HEADER = 128;  // ticket lives in its own 128-byte line
+constexpr int RED_GROUP = 128;  // blocks per first-level group of the finish
+constexpr int RED_MAX_GROUPS = RED_MAX_PARTIALS / RED_GROUP;
+// Workspace layout (zeroed once by the caller): the global ticket in its own
+// 128-byte line, the block partials (up to 16 bytes each), the group tickets,
+// the group partials.
+constexpr size_t RED_HEADER = 128;
+constexpr size_t RED_GTICKET_OFF = RED_HEADER + (size_t)RED_MAX_PARTIALS * 16;
+constexpr size_t RED_GPART_OFF = RED_GTICKET_OFF + (size_t)RED_MAX_GROUPS * 4;
+constexpr size_t RED_WS_BYTES = RED_GPART_OFF + (size_t)RED_MAX_GROUPS * 16;
 
 template <typename T>
 __host__ __device__ constexpr bool is_fp() {
@@ -142,40 +150,70 @@ __device__ __forceinline__ T block_fold(T v, T *smem) {
   return v;
 }
 
-// Grid finish (§8(a) a4), called by every thread of every block with the
-// block's partial v (valid in thread 0): the partial goes to the workspace,
-// then __threadfence + an atomic ticket; the block drawing the last ticket
-// folds all partials in index order, resets the ticket (reusable by the next
-// call), runs the cross-GPU exchange if any, and writes *out.
+// Fold vals[0..count) (L2 reads, bypassing L1) over the block; result valid
+// in thread 0.  Thread t folds t, t + BLOCK, ... in index order with 8
+// independent loads in flight, then the fixed block tree.
 template <int OP, int BLOCK, typename Tacc>
-__device__ __forceinline__ void grid_finish(Tacc v, Tacc *smem, Tacc *partials, unsigned int *ticket, Tacc *out,
-                                            const Exchange &xg) {
-  __shared__ bool is_last;
-  if (threadIdx.x == 0) {
-    partials[blockIdx.x] = v;
-    __threadfence();
-    is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!is_last) return;
-
-  // Last block: fold the partials in index order (L2 reads, bypassing L1).
-  __threadfence();
-  // 8 independent L2 loads per thread in flight (a dependent one-by-one loop
-  // over up to 64 partials per thread cost several microseconds of tail).
+__device__ __forceinline__ Tacc fold_range(const Tacc *vals, int count, Tacc *smem) {
   Tacc w = Op<OP, Tacc>::neutral();
-  for (int base = threadIdx.x; base < (int)gridDim.x; base += BLOCK * 8) {
+  for (int base = threadIdx.x; base < count; base += BLOCK * 8) {
     Tacc u[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int i = base + j * BLOCK;
-      u[j] = i < (int)gridDim.x ? ldcg<Tacc>(partials + i) : Op<OP, Tacc>::neutral();
+      u[j] = i < count ? ldcg<Tacc>(vals + i) : Op<OP, Tacc>::neutral();
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) w = Op<OP, Tacc>::fold(w, u[j]);
   }
   __syncthreads();  // smem reuse
-  w = block_fold<OP, BLOCK, Tacc>(w, smem);
+  return block_fold<OP, BLOCK, Tacc>(w, smem);
+}
+
+// Grid finish (§8(a) a4), called by every thread of every block with the
+// block's partial v (valid in thread 0).  Two-level last-block-done: blocks
+// form groups of RED_GROUP consecutive ids; a block writes its partial, then
+// __threadfence + the group's atomic ticket; the block drawing a group's last
+// ticket folds that group's partials in index order into a group partial and
+// takes the global ticket; the block drawing the last global ticket folds
+// the group partials in group order, resets the tickets (reusable by the
+// next call), runs the cross-GPU exchange if any, and writes *out.  With one
+// group the global level is skipped.  The tail after the last data load is
+// two short L2 folds (<= RED_GROUP and <= RED_MAX_GROUPS values) instead of
+// one fold over up to RED_MAX_PARTIALS partials (16 dependent L2 rounds at
+// 32768 partials: ~10 us).  Every fold order depends on the grid only.
+template <int OP, int BLOCK, typename Tacc>
+__device__ __forceinline__ void grid_finish(Tacc v, Tacc *smem, Tacc *partials, unsigned int *ticket, Tacc *out,
+                                            const Exchange &xg) {
+  __shared__ bool is_last_in_group, is_last;
+  const int grid = (int)gridDim.x;
+  const int ngroups = (grid + RED_GROUP - 1) / RED_GROUP;
+  const int g = (int)blockIdx.x / RED_GROUP;
+  const int gsize = min(RED_GROUP, grid - g * RED_GROUP);
+  unsigned int *gticket = reinterpret_cast<unsigned int *>(reinterpret_cast<char *>(ticket) + RED_GTICKET_OFF);
+  Tacc *gpart = reinterpret_cast<Tacc *>(reinterpret_cast<char *>(ticket) + RED_GPART_OFF);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = v;
+    __threadfence();
+    is_last_in_group = atomicAdd(ngroups == 1 ? ticket : gticket + g, 1u) == (unsigned)gsize - 1;
+  }
+  __syncthreads();
+  if (!is_last_in_group) return;
+
+  __threadfence();
+  Tacc w = fold_range<OP, BLOCK, Tacc>(partials + g * RED_GROUP, gsize, smem);
+  if (ngroups > 1) {
+    if (threadIdx.x == 0) {
+      gticket[g] = 0u;
+      gpart[g] = w;
+      __threadfence();
+      is_last = atomicAdd(ticket, 1u) == (unsigned)ngroups - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    w = fold_range<OP, BLOCK, Tacc>(gpart, ngroups, smem);
+  }
   if (threadIdx.x == 0) {
     *ticket = 0u;
     if (xg.world > 0) w = exchange_fold<OP, Tacc>(xg, w);

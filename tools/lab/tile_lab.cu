@@ -25,7 +25,17 @@ static int run(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   X(5, int32_t, 32, 16, 8, 8, 16)   \
   X(6, int32_t, 24, 64, 8, 8, 16)   \
   X(20, int64_t, 24, 32, 8, 4, 8)   \
-  X(21, int64_t, 24, 32, 8, 4, 16)
+  X(21, int64_t, 24, 32, 8, 4, 16)   \
+  X(10, int32_t, 12, 32, 8, 8, 8)   \
+  X(11, int32_t, 12, 64, 8, 8, 8)   \
+  X(12, int32_t, 8, 32, 8, 8, 8)    \
+  X(13, int32_t, 8, 48, 8, 8, 8)    \
+  X(14, int32_t, 12, 48, 8, 8, 8)   \
+  X(15, int32_t, 8, 64, 8, 8, 8)    \
+  X(16, int32_t, 12, 16, 8, 8, 8)   \
+  X(22, int64_t, 12, 32, 8, 4, 8)   \
+  X(23, int64_t, 12, 64, 8, 4, 8)   \
+  X(24, int64_t, 8, 32, 8, 4, 8)
 
 extern "C" int lab_scan(int v, int64_t n, const void *in, void *out, void *ws, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
