@@ -24,7 +24,7 @@
 // load one halo element each (computing p' there from r and p, the same
 // bits).  The dot products accumulate per vector lane, fold in the fixed lane
 // tree / warp butterfly / block order and finish in the last block
-// (red_detail::grid_finish), like reduce_kernel.  Arrays not 32-byte aligned
+// (red_detail::grid_finish, tagged slots), like reduce_kernel.  Arrays not 32-byte aligned
 // take a scalar grid-stride loop (same arithmetic).
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -81,14 +81,14 @@ ga_status_t run_direction(int64_t n, const ga_dscalar_t &beta, const void *r, co
   a.pout = static_cast<T *>(pout);
   a.ap = static_cast<T *>(ap);
   a.out = static_cast<T *>(pap);
-  a.ticket = static_cast<unsigned int *>(ws);
-  a.partials = reinterpret_cast<T *>(static_cast<char *>(ws) + RED_HEADER);
   const bool vec = aligned32(r) && aligned32(pin) && aligned32(pout) && aligned32(ap) && (!diag || aligned32(diag));
   a.nvec = vec ? n / VEC : 0;
+  const int grid = grid_for(n, a.nvec, DIR_UNROLL);
+  a.fin = make_finish(ws, grid, DIR_MINB);
   if (diag)
-    cg_direction_kernel<T, DIR_UNROLL, DIR_MINB, true><<<grid_for(n, a.nvec, DIR_UNROLL), CG_BLOCK, 0, s>>>(a);
+    cg_direction_kernel<T, DIR_UNROLL, DIR_MINB, true><<<grid, CG_BLOCK, 0, s>>>(a);
   else
-    cg_direction_kernel<T, DIR_UNROLL, DIR_MINB, false><<<grid_for(n, a.nvec, DIR_UNROLL), CG_BLOCK, 0, s>>>(a);
+    cg_direction_kernel<T, DIR_UNROLL, DIR_MINB, false><<<grid, CG_BLOCK, 0, s>>>(a);
   count_launch();
   return check_launch("cg_direction_kernel");
 }
@@ -107,11 +107,11 @@ ga_status_t run_update(int64_t n, const ga_dscalar_t &alpha, void *x, void *r, c
   a.p = static_cast<const T *>(p);
   a.ap = static_cast<const T *>(ap);
   a.out = static_cast<T *>(rr);
-  a.ticket = static_cast<unsigned int *>(ws);
-  a.partials = reinterpret_cast<T *>(static_cast<char *>(ws) + RED_HEADER);
   const bool vec = aligned32(x) && aligned32(r) && aligned32(p) && aligned32(ap);
   a.nvec = vec ? n / VEC : 0;
-  cg_update_kernel<T, UPD_UNROLL, UPD_MINB><<<grid_for(n, a.nvec, UPD_UNROLL), CG_BLOCK, 0, s>>>(a);
+  const int grid = grid_for(n, a.nvec, UPD_UNROLL);
+  a.fin = make_finish(ws, grid, UPD_MINB);
+  cg_update_kernel<T, UPD_UNROLL, UPD_MINB><<<grid, CG_BLOCK, 0, s>>>(a);
   count_launch();
   return check_launch("cg_update_kernel");
 }

@@ -26,8 +26,8 @@ struct DirArgs {
   const T *diag;              // nullptr: constant d
   const T *r, *pin;
   T *pout, *ap;
-  T *out, *partials;
-  unsigned int *ticket;
+  T *out;
+  Finish fin;
 };
 
 template <typename T>
@@ -37,8 +37,8 @@ struct UpdArgs {
   const T *anum, *aden;
   T *x, *r;
   const T *p, *ap;
-  T *out, *partials;
-  unsigned int *ticket;
+  T *out;
+  Finish fin;
 };
 
 // p' = RN(RN(1*r) + RN(beta*p)) — gpuarray_axpbyz(1, r, beta, p) (R1).
@@ -74,6 +74,7 @@ template <typename T, int CG_UNROLL, int CG_MINB, bool DIAG>
 __global__ void __launch_bounds__(CG_BLOCK, CG_MINB) cg_direction_kernel(DirArgs<T> a) {
   constexpr int VEC = 32 / sizeof(T);
   __shared__ T smem[CG_BLOCK / 32];
+  const uint32_t tag = finish_tag(a.fin);
   const int lane = threadIdx.x & 31;
   const T beta = coef(a.bscale, a.bnum, a.bden);
   T acc[VEC];
@@ -141,13 +142,14 @@ __global__ void __launch_bounds__(CG_BLOCK, CG_MINB) cg_direction_kernel(DirArgs
     }
   }
   const T v = block_fold<GA_OP_SUM, CG_BLOCK, T>(lane_tree<T, VEC>(acc), smem);
-  grid_finish<GA_OP_SUM, CG_BLOCK, T>(v, smem, a.partials, a.ticket, a.out, Exchange{});
+  grid_finish<GA_OP_SUM, CG_BLOCK, T>(v, tag, smem, a.fin, a.out, Exchange{});
 }
 
 template <typename T, int CG_UNROLL, int CG_MINB>
 __global__ void __launch_bounds__(CG_BLOCK, CG_MINB) cg_update_kernel(UpdArgs<T> a) {
   constexpr int VEC = 32 / sizeof(T);
   __shared__ T smem[CG_BLOCK / 32];
+  const uint32_t tag = finish_tag(a.fin);
   // x' = RN(RN(1*x) + RN(alpha*p)), r' = RN(RN(1*r) + RN(-alpha*ap)):
   // gpuarray_axpbyz_ds(1, x, alpha, p) and (1, r, -alpha, ap), whose b
   // factors are RN(+-ascale * q) = +-alpha exactly.
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(CG_BLOCK, CG_MINB) cg_update_kernel(UpdArgs<T>
     }
   }
   const T v = block_fold<GA_OP_SUM, CG_BLOCK, T>(lane_tree<T, VEC>(acc), smem);
-  grid_finish<GA_OP_SUM, CG_BLOCK, T>(v, smem, a.partials, a.ticket, a.out, Exchange{});
+  grid_finish<GA_OP_SUM, CG_BLOCK, T>(v, tag, smem, a.fin, a.out, Exchange{});
 }
 
 }  // namespace cg_detail

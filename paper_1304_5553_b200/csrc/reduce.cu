@@ -15,13 +15,13 @@
 //      tools/lab/red_lab.cu; the CTA shape is from red_shape_lab.cu);
 //   2. fixed-order lane tree -> warp xor-butterfly -> per-warp partial in
 //      shared memory -> warp 0 folds the block partial;
-//   3. last-block-done finish, two levels: the block partial goes to
-//      workspace, then __threadfence + its group's atomic ticket (groups of
-//      128 consecutive blocks); the block that draws a group's last ticket
-//      folds the group in index order and takes the global ticket; the block
-//      that draws the last one folds the group partials in order, writes
-//      *out and resets the tickets (no second launch, no host sync, no
-//      memset between calls).
+//   3. single-pass finish, two levels (red_detail::grid_finish): a block
+//      publishes its partial into a slot tagged with the call's epoch and
+//      exits (no fence, no atomic); the last block of each group of 128
+//      waits for its group's slots and folds them in index order; the last
+//      block of the grid folds the group partials in order, writes *out and
+//      advances the epoch (no second launch, no host sync, no memset
+//      between calls).
 // Deterministic for a given n (the grid depends on n only, not on the
 // device): every fold order above is fixed.
 #include <cuda_runtime.h>
@@ -59,8 +59,6 @@ ga_status_t run(int64_t n, const void *x, const void *y, void *out, void *ws, co
   p.x = static_cast<const Tin *>(x);
   p.y = static_cast<const Tin *>(y);
   p.out = static_cast<Tacc *>(out);
-  p.ticket = static_cast<unsigned int *>(ws);
-  p.partials = reinterpret_cast<Tacc *>(static_cast<char *>(ws) + RED_HEADER);
   p.xg = xg;
 
   const uintptr_t phase = (uintptr_t)x & 31;
@@ -78,6 +76,7 @@ ga_status_t run(int64_t n, const void *x, const void *y, void *out, void *ws, co
   // the unaligned path), capped at RED_MAX_PARTIALS
   const int64_t units = coaligned ? cdiv(std::max<int64_t>(p.nvec, 1), (int64_t)RED_BLOCK * UNROLL) : cdiv(n, RED_BLOCK);
   const int grid = (int)std::max<int64_t>(std::min<int64_t>(units, RED_MAX_PARTIALS), 1);
+  p.fin = make_finish(ws, grid, RED_MINB);
   kern<<<grid, RED_BLOCK, 0, s>>>(p);
   count_launch();
   return check_launch("reduce_kernel");

@@ -5,6 +5,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string.h>
+
+#include <algorithm>
 #include <type_traits>
 
 #include "ga_device.cuh"
@@ -15,15 +18,38 @@ namespace red_detail {
 
 
 constexpr int RED_MAX_PARTIALS = 32768;
-constexpr int RED_GROUP = 128;  // blocks per first-level group of the finish
-constexpr int RED_MAX_GROUPS = RED_MAX_PARTIALS / RED_GROUP;
-// Workspace layout (zeroed once by the caller): the global ticket in its own
-// 128-byte line, the block partials (up to 16 bytes each), the group tickets,
-// the group partials.
+constexpr int RED_GROUP = 128;  // blocks per first-level group of the finish (at least)
+constexpr int RED_MAX_GROUPS = 256;
+// Workspace layout (zeroed once by the caller): the call epoch (u32) in its
+// own 128-byte line, then one 32-byte slot per block partial, then one per
+// group partial.  A slot holds the value (<= 16 bytes) and the tag of the
+// call that wrote it (see grid_finish).
 constexpr size_t RED_HEADER = 128;
-constexpr size_t RED_GTICKET_OFF = RED_HEADER + (size_t)RED_MAX_PARTIALS * 16;
-constexpr size_t RED_GPART_OFF = RED_GTICKET_OFF + (size_t)RED_MAX_GROUPS * 4;
-constexpr size_t RED_WS_BYTES = RED_GPART_OFF + (size_t)RED_MAX_GROUPS * 16;
+constexpr size_t RED_SLOT = 32;
+constexpr size_t RED_GSLOT_OFF = RED_HEADER + (size_t)RED_MAX_PARTIALS * RED_SLOT;
+constexpr size_t RED_WS_BYTES = RED_GSLOT_OFF + (size_t)RED_MAX_GROUPS * RED_SLOT;
+constexpr uint32_t RED_EPOCH_MASK = 0x7fffffffu;
+
+// What a kernel needs to finish: the workspace and the group size (host:
+// finish_group()).
+struct Finish {
+  char *ws;
+  int group;
+};
+
+// Host: the finish of a `grid`-block launch of a kernel with at least
+// `minb` co-resident blocks per SM.  Groups of RED_GROUP blocks (more when
+// the grid would need over RED_MAX_GROUPS groups), and fewer groups than
+// co-resident blocks so that the waiting group leaders can never starve the
+// blocks they wait for (every full B200 launch: 128).
+inline Finish make_finish(void *ws, int64_t grid, int minb) {
+  const int64_t resident = (int64_t)sm_count() * minb;
+  const int64_t max_groups = std::max<int64_t>(1, std::min<int64_t>(RED_MAX_GROUPS, resident - 1));
+  Finish f;
+  f.ws = static_cast<char *>(ws);
+  f.group = (int)std::max<int64_t>(RED_GROUP, (grid + max_groups - 1) / max_groups);
+  return f;
+}
 
 template <typename T>
 __host__ __device__ constexpr bool is_fp() {
@@ -85,8 +111,7 @@ struct RedArgs {
   const Tin *x;
   const Tin *y;
   Tacc *out;
-  Tacc *partials;
-  unsigned int *ticket;
+  Finish fin;
   Exchange xg;  // cross-GPU finish (world == 0: none)
 };
 
@@ -150,74 +175,119 @@ __device__ __forceinline__ T block_fold(T v, T *smem) {
   return v;
 }
 
-// Fold vals[0..count) (L2 reads, bypassing L1) over the block; result valid
-// in thread 0.  Thread t folds t, t + BLOCK, ... in index order with 8
-// independent loads in flight, then the fixed block tree.
-template <int OP, int BLOCK, typename Tacc>
-__device__ __forceinline__ Tacc fold_range(const Tacc *vals, int count, Tacc *smem) {
-  Tacc w = Op<OP, Tacc>::neutral();
-  for (int base = threadIdx.x; base < count; base += BLOCK * 8) {
-    Tacc u[8];
+// Tagged partial slots.  The tag of a call is its epoch + 1 (never 0, so a
+// zeroed workspace holds no valid slot).  A value of S bytes is stored as
+// S/4 64-bit words {tag:32 | 32 value bits}, each written with one relaxed
+// 64-bit store (single-copy atomic) and read with relaxed loads: a reader that
+// sees the call's tag in every word holds that call's value — no fence, no
+// atomic, no release/acquire pair on either side.
+__device__ __forceinline__ uint32_t finish_tag(const Finish &f) {
+  uint32_t e;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(e) : "l"(f.ws) : "memory");
+  return (e & RED_EPOCH_MASK) + 1u;
+}
+
+template <typename Tacc>
+__device__ __forceinline__ void slot_publish(char *slot, uint32_t tag, Tacc v) {
+  constexpr int W = sizeof(Tacc) / 4;
+  static_assert(W * 4 == sizeof(Tacc) && W * 8 <= RED_SLOT, "slot holds up to 16-byte values");
+  uint32_t bits[W];
+  memcpy(bits, &v, sizeof(Tacc));
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int i = base + j * BLOCK;
-      u[j] = i < count ? ldcg<Tacc>(vals + i) : Op<OP, Tacc>::neutral();
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) w = Op<OP, Tacc>::fold(w, u[j]);
+  for (int k = 0; k < W; ++k) {
+    const uint64_t w = ((uint64_t)tag << 32) | bits[k];
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(slot + 8 * k), "l"(w) : "memory");
   }
+}
+
+// Spin (with a short sleep between polls) until every word of the slot
+// carries `tag`, then return the value.  A slot that never arrives (a block
+// that cannot run) traps after 10 s instead of hanging.
+template <typename Tacc>
+__device__ __forceinline__ Tacc slot_wait(const char *slot, uint32_t tag) {
+  constexpr int W = sizeof(Tacc) / 4;
+  uint32_t bits[W];
+  uint32_t spins = 0;
+  uint64_t t0 = 0;
+  while (true) {
+    bool ready = true;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      uint64_t w;
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(slot + 8 * k) : "memory");
+      ready = ready && (uint32_t)(w >> 32) == tag;
+      bits[k] = (uint32_t)w;
+    }
+    if (ready) break;
+    __nanosleep(64);
+    if ((++spins & 1023u) == 0) {
+      uint64_t now;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 10000000000ull) __trap();
+    }
+  }
+  Tacc v;
+  memcpy(&v, bits, sizeof(Tacc));
+  return v;
+}
+
+// Fold slots [0, count) of `base` in a fixed order — thread t folds t,
+// t + BLOCK, ... then the block tree — with slot count-1 replaced by `own`
+// (the caller's value, which it never published).  Result valid in thread 0.
+template <int OP, int BLOCK, typename Tacc>
+__device__ __forceinline__ Tacc fold_slots(const char *base, int count, uint32_t tag, Tacc own, Tacc *smem) {
+  Tacc w = Op<OP, Tacc>::neutral();
+  for (int i = threadIdx.x; i < count; i += BLOCK)
+    w = Op<OP, Tacc>::fold(w, i == count - 1 ? own : slot_wait<Tacc>(base + (size_t)i * RED_SLOT, tag));
   __syncthreads();  // smem reuse
   return block_fold<OP, BLOCK, Tacc>(w, smem);
 }
 
 // Grid finish (§8(a) a4), called by every thread of every block with the
-// block's partial v (valid in thread 0).  Two-level last-block-done: blocks
-// form groups of RED_GROUP consecutive ids; a block writes its partial, then
-// __threadfence + the group's atomic ticket; the block drawing a group's last
-// ticket folds that group's partials in index order into a group partial and
-// takes the global ticket; the block drawing the last global ticket folds
-// the group partials in group order, resets the tickets (reusable by the
-// next call), runs the cross-GPU exchange if any, and writes *out.  With one
-// group the global level is skipped.  The tail after the last data load is
-// two short L2 folds (<= RED_GROUP and <= RED_MAX_GROUPS values) instead of
-// one fold over up to RED_MAX_PARTIALS partials (16 dependent L2 rounds at
-// 32768 partials: ~10 us).  Every fold order depends on the grid only.
+// block's partial v (valid in thread 0) and the call's tag (finish_tag,
+// loaded at kernel start).  Blocks form groups of f.group consecutive ids.
+// A block that is not the last of its group publishes its partial into its
+// tagged slot and exits — no fence, no atomic, no wait.  The LAST block of a
+// group waits for the group's slots and folds them in index order (its own
+// partial last); the last block of the grid then waits for the group
+// partials, folds them in group order, runs the cross-GPU exchange if any,
+// writes *out and advances the epoch (stream order makes it visible to the
+// next call).  With one group the second level is skipped.  Only group
+// leaders wait, and only for blocks that never wait, so progress needs more
+// co-resident blocks than groups (finish_group() guarantees it; a starved
+// wait traps after 10 s).  Every fold order depends on (grid, group) only.
 template <int OP, int BLOCK, typename Tacc>
-__device__ __forceinline__ void grid_finish(Tacc v, Tacc *smem, Tacc *partials, unsigned int *ticket, Tacc *out,
+__device__ __forceinline__ void grid_finish(Tacc v, uint32_t tag, Tacc *smem, const Finish &f, Tacc *out,
                                             const Exchange &xg) {
-  __shared__ bool is_last_in_group, is_last;
-  const int grid = (int)gridDim.x;
-  const int ngroups = (grid + RED_GROUP - 1) / RED_GROUP;
-  const int g = (int)blockIdx.x / RED_GROUP;
-  const int gsize = min(RED_GROUP, grid - g * RED_GROUP);
-  unsigned int *gticket = reinterpret_cast<unsigned int *>(reinterpret_cast<char *>(ticket) + RED_GTICKET_OFF);
-  Tacc *gpart = reinterpret_cast<Tacc *>(reinterpret_cast<char *>(ticket) + RED_GPART_OFF);
-  if (threadIdx.x == 0) {
-    partials[blockIdx.x] = v;
-    __threadfence();
-    is_last_in_group = atomicAdd(ngroups == 1 ? ticket : gticket + g, 1u) == (unsigned)gsize - 1;
+  __shared__ Tacc s_own;
+  const int grid = (int)gridDim.x, b = (int)blockIdx.x;
+  const int ngroups = (grid + f.group - 1) / f.group;
+  const int g = b / f.group;
+  const int gsize = min(f.group, grid - g * f.group);
+  char *slots = f.ws + RED_HEADER;
+  char *gslots = f.ws + RED_GSLOT_OFF;
+  if (b != g * f.group + gsize - 1) {
+    if (threadIdx.x == 0) slot_publish<Tacc>(slots + (size_t)b * RED_SLOT, tag, v);
+    return;
   }
+  if (threadIdx.x == 0) s_own = v;
   __syncthreads();
-  if (!is_last_in_group) return;
-
-  __threadfence();
-  Tacc w = fold_range<OP, BLOCK, Tacc>(partials + g * RED_GROUP, gsize, smem);
+  Tacc w = fold_slots<OP, BLOCK, Tacc>(slots + (size_t)g * f.group * RED_SLOT, gsize, tag, s_own, smem);
   if (ngroups > 1) {
-    if (threadIdx.x == 0) {
-      gticket[g] = 0u;
-      gpart[g] = w;
-      __threadfence();
-      is_last = atomicAdd(ticket, 1u) == (unsigned)ngroups - 1;
+    if (b != grid - 1) {
+      if (threadIdx.x == 0) slot_publish<Tacc>(gslots + (size_t)g * RED_SLOT, tag, w);
+      return;
     }
+    __syncthreads();  // every thread has read s_own
+    if (threadIdx.x == 0) s_own = w;
     __syncthreads();
-    if (!is_last) return;
-    __threadfence();
-    w = fold_range<OP, BLOCK, Tacc>(gpart, ngroups, smem);
+    w = fold_slots<OP, BLOCK, Tacc>(gslots, ngroups, tag, s_own, smem);
   }
   if (threadIdx.x == 0) {
-    *ticket = 0u;
     if (xg.world > 0) w = exchange_fold<OP, Tacc>(xg, w);
     *out = w;
+    *reinterpret_cast<volatile uint32_t *>(f.ws) = tag & RED_EPOCH_MASK;  // the next call's epoch
   }
 }
 
@@ -227,6 +297,7 @@ __global__ void __launch_bounds__(RED_BLOCK, MINB) reduce_kernel(RedArgs<Tin, Ta
   constexpr bool HAS_Y = MAP == GA_MAP_MUL || MAP == GA_MAP_CONJ_MUL;
   __shared__ Tacc smem[RED_BLOCK / 32];
 
+  const uint32_t tag = finish_tag(p.fin);
   const int64_t tid = (int64_t)blockIdx.x * RED_BLOCK + threadIdx.x;
   const int64_t nthreads = (int64_t)gridDim.x * RED_BLOCK;
 
@@ -296,7 +367,7 @@ __global__ void __launch_bounds__(RED_BLOCK, MINB) reduce_kernel(RedArgs<Tin, Ta
   }
   Tacc v = block_fold<OP, RED_BLOCK, Tacc>(acc[0], smem);
 
-  grid_finish<OP, RED_BLOCK, Tacc>(v, smem, p.partials, p.ticket, p.out, p.xg);
+  grid_finish<OP, RED_BLOCK, Tacc>(v, tag, smem, p.fin, p.out, p.xg);
 }
 
 template <typename Tacc, int OP>

@@ -77,7 +77,7 @@ def _ptr(t):
 
 # --------------------------------------------------------------- workspaces
 # One zero-filled workspace per (kernel family, device, stream); the kernels
-# keep it valid across calls (self-resetting ticket / epoch-tagged scan
+# keep it valid across calls (epoch-tagged reduce slots / epoch-tagged scan
 # status), so it is zeroed once at allocation and never again.  Reduce and
 # scan workspaces have different layouts and are never shared.
 _ws = {}

@@ -45,7 +45,7 @@ def test_version_and_strings(abi):
 
 
 def test_workspace_sizes(abi):
-    assert abi.gpuarray_reduce_workspace_bytes(abi.GA_F32, 1 << 30) == 128 + 16 * 32768
+    assert abi.gpuarray_reduce_workspace_bytes(abi.GA_F32, 1 << 30) == 128 + 32 * 32768 + 32 * 256
     assert abi.gpuarray_xgpu_buffer_bytes() == 2 * 64 * 32
     a = abi.gpuarray_scan_workspace_bytes(abi.GA_I32, 1 << 30)
     assert a == 256 + 8 * ((1 << 30) // 4096)

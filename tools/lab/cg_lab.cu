@@ -32,8 +32,7 @@ static int dir(int64_t n, const float *r, const float *pin, float *pout, float *
   a.pout = pout;
   a.ap = ap;
   a.out = out;
-  a.ticket = static_cast<unsigned int *>(ws);
-  a.partials = reinterpret_cast<float *>(static_cast<char *>(ws) + RED_HEADER);
+  a.fin = Finish{(char *)ws, RED_GROUP};  // = make_finish on a full B200
   cg_direction_kernel<float, U, M, false><<<grid_for(a.nvec, U * LP), CG_BLOCK, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
@@ -52,8 +51,7 @@ static int upd(int64_t n, float *x, float *r, const float *p, const float *ap, f
   a.p = p;
   a.ap = ap;
   a.out = out;
-  a.ticket = static_cast<unsigned int *>(ws);
-  a.partials = reinterpret_cast<float *>(static_cast<char *>(ws) + RED_HEADER);
+  a.fin = Finish{(char *)ws, RED_GROUP};  // = make_finish on a full B200
   cg_update_kernel<float, U, M><<<grid_for(a.nvec, U * LP), CG_BLOCK, 0, s>>>(a);
   return (int)cudaGetLastError();
 }
