@@ -53,7 +53,16 @@ ga_status_t run(int64_t n, const void *x, const void *y, void *out, void *ws, co
     return check_launch("neutral_kernel");
   }
   constexpr int VEC = 32 / sizeof(Tin);
-  constexpr int UNROLL = (MAP == GA_MAP_MUL || MAP == GA_MAP_CONJ_MUL) ? 4 : 8;
+  // Vectors in flight per thread: 8 (4 per input for x*y); half of that
+  // where the per-vector work needs more registers — widening accumulators,
+  // integer products, MAX/MIN over a product (guarded, no neutral fill) —
+  // so that the instances stay within the 64 registers of 4 CTAs/SM
+  // without spilling (ptxas -v: 0 bytes for every instance).
+  constexpr bool WIDEN = sizeof(Tacc) > sizeof(Tin);
+  constexpr bool INT_PRODUCT = !is_fp<Tacc>() && MAP != GA_MAP_ID;
+  constexpr int DIV = (WIDEN || (INT_PRODUCT && sizeof(Tacc) == 8)) ? 4
+                      : (INT_PRODUCT || (OP != GA_OP_SUM && MAP != GA_MAP_ID)) ? 2 : 1;
+  constexpr int UNROLL = std::max(1, ((MAP == GA_MAP_MUL || MAP == GA_MAP_CONJ_MUL) ? 4 : 8) / DIV);
   RedArgs<Tin, Tacc> p;
   p.n = n;
   p.x = static_cast<const Tin *>(x);

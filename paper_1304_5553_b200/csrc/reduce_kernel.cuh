@@ -25,7 +25,7 @@ constexpr int RED_MAX_GROUPS = 256;
 // group partial.  A slot holds the value (<= 16 bytes) and the tag of the
 // call that wrote it (see grid_finish).
 constexpr size_t RED_HEADER = 128;
-constexpr size_t RED_SLOT = 32;
+constexpr size_t RED_SLOT = 32;  // the largest slot (16-byte values); see slot_stride
 constexpr size_t RED_GSLOT_OFF = RED_HEADER + (size_t)RED_MAX_PARTIALS * RED_SLOT;
 constexpr size_t RED_WS_BYTES = RED_GSLOT_OFF + (size_t)RED_MAX_GROUPS * RED_SLOT;
 constexpr uint32_t RED_EPOCH_MASK = 0x7fffffffu;
@@ -187,6 +187,13 @@ __device__ __forceinline__ uint32_t finish_tag(const Finish &f) {
   return (e & RED_EPOCH_MASK) + 1u;
 }
 
+// Slots are packed at their own size (2 x sizeof(Tacc): one 8-byte word per
+// 4 value bytes), so consecutive blocks fill whole 32-byte sectors.
+template <typename Tacc>
+__host__ __device__ constexpr size_t slot_stride() {
+  return 2 * sizeof(Tacc);
+}
+
 template <typename Tacc>
 __device__ __forceinline__ void slot_publish(char *slot, uint32_t tag, Tacc v) {
   constexpr int W = sizeof(Tacc) / 4;
@@ -239,7 +246,7 @@ template <int OP, int BLOCK, typename Tacc>
 __device__ __forceinline__ Tacc fold_slots(const char *base, int count, uint32_t tag, Tacc own, Tacc *smem) {
   Tacc w = Op<OP, Tacc>::neutral();
   for (int i = threadIdx.x; i < count; i += BLOCK)
-    w = Op<OP, Tacc>::fold(w, i == count - 1 ? own : slot_wait<Tacc>(base + (size_t)i * RED_SLOT, tag));
+    w = Op<OP, Tacc>::fold(w, i == count - 1 ? own : slot_wait<Tacc>(base + (size_t)i * slot_stride<Tacc>(), tag));
   __syncthreads();  // smem reuse
   return block_fold<OP, BLOCK, Tacc>(w, smem);
 }
@@ -268,15 +275,15 @@ __device__ __forceinline__ void grid_finish(Tacc v, uint32_t tag, Tacc *smem, co
   char *slots = f.ws + RED_HEADER;
   char *gslots = f.ws + RED_GSLOT_OFF;
   if (b != g * f.group + gsize - 1) {
-    if (threadIdx.x == 0) slot_publish<Tacc>(slots + (size_t)b * RED_SLOT, tag, v);
+    if (threadIdx.x == 0) slot_publish<Tacc>(slots + (size_t)b * slot_stride<Tacc>(), tag, v);
     return;
   }
   if (threadIdx.x == 0) s_own = v;
   __syncthreads();
-  Tacc w = fold_slots<OP, BLOCK, Tacc>(slots + (size_t)g * f.group * RED_SLOT, gsize, tag, s_own, smem);
+  Tacc w = fold_slots<OP, BLOCK, Tacc>(slots + (size_t)g * f.group * slot_stride<Tacc>(), gsize, tag, s_own, smem);
   if (ngroups > 1) {
     if (b != grid - 1) {
-      if (threadIdx.x == 0) slot_publish<Tacc>(gslots + (size_t)g * RED_SLOT, tag, w);
+      if (threadIdx.x == 0) slot_publish<Tacc>(gslots + (size_t)g * slot_stride<Tacc>(), tag, w);
       return;
     }
     __syncthreads();  // every thread has read s_own

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "ga_host.h"
 #include "scan_kernel.cuh"
@@ -22,14 +23,18 @@ using namespace scan_detail;
 //   M  32 warps x 8 rows (128 KiB) when that gives at least M_MIN_TILES;
 //   S  8 warps (16 for 8-byte T) x 8 rows otherwise: enough tiles to spread
 //      a small array over the SMs.
-// Every warp keeps 8 rows of 512 bytes in flight (UNROLL 8); the look-back
+// Every warp keeps 8 rows of 512 bytes in flight in phase 1 (P1U) and
+// UNROLL rows in phase 3: 8 for 4-byte types and exclusive int64 at the L
+// shape, 4 for the other 8-byte scans, 2 for widened ones, which keeps every instance spill-free (ptxas -v) — widened
+// scans 10-14% faster at 2^28-2^30 and int64 inclusive 3% faster than with
+// 8 rows and spills (tools/lab/ab_scan.py); the look-back
 // reads 8 (4 for 8-byte T) predecessors per lane per round trip; warps 1..
 // load and locally scan their first phase-3 rows while warp 0 looks back.
 // RG: the register-tile fallback for arrays that are not 16-byte aligned
 // (32-byte for a widened output): 256 threads x 16 scalar-loaded items.
 enum Shape { SHAPE_S = 0, SHAPE_M = 1, SHAPE_L = 2, SHAPE_RG = 3 };
 constexpr int64_t L_MIN_TILES = 256, M_MIN_TILES = 64;
-constexpr int UNROLL = 8, DEPTH4 = 8, DEPTH8 = 4;
+constexpr int UNROLL4 = 8, UNROLL8 = 4, UNROLLW = 2, P1U = 8, DEPTH4 = 8, DEPTH8 = 4;
 constexpr int RG_BLOCK = 256, RG_ITEMS = 16, RG_DEPTH = 4;
 
 
@@ -71,10 +76,13 @@ ga_status_t run(int64_t n, const void *in, void *out, const void *carry, int64_t
   } else {
     constexpr int W = ShapeOf<SHAPE, T>::WARPS, R = ShapeOf<SHAPE, T>::ROWS;
     constexpr int D = sizeof(T) == 8 ? DEPTH8 : DEPTH4;
+    // exclusive int64 at the L shape fits 8 rows without spilling (and is 3% faster with them)
+    constexpr bool ROWS8 = sizeof(T) == 4 || (EXCLUSIVE && SHAPE == SHAPE_L && std::is_integral<T>::value);
+    constexpr int U = sizeof(T) != sizeof(Tin) ? UNROLLW : ROWS8 ? UNROLL4 : UNROLL8;
     if (in == out)
-      scan_l2_kernel<OP, T, Tin, W, R, UNROLL, D, false, EXCLUSIVE, true><<<grid, W * 32, 0, s>>>(p);
+      scan_l2_kernel<OP, T, Tin, W, R, U, D, false, EXCLUSIVE, true, P1U><<<grid, W * 32, 0, s>>>(p);
     else
-      scan_l2_kernel<OP, T, Tin, W, R, UNROLL, D, true, EXCLUSIVE, true><<<grid, W * 32, 0, s>>>(p);
+      scan_l2_kernel<OP, T, Tin, W, R, U, D, true, EXCLUSIVE, true, P1U><<<grid, W * 32, 0, s>>>(p);
   }
   count_launch();
   return check_launch("scan_kernel");

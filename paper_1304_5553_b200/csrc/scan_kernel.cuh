@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p)
 // BLOCK x ITEMS consecutive elements per CTA, scalar loads/stores.
 // ===========================================================================
 template <int OP, typename T, typename Tin, int BLOCK, int ITEMS, int DEPTH, bool EXCLUSIVE>
-__global__ void __launch_bounds__(BLOCK) scan_reg_kernel(ScanArgs<T, Tin> p) {
+__global__ void __launch_bounds__(BLOCK, 2) scan_reg_kernel(ScanArgs<T, Tin> p) {
   using O = Op<OP, T>;
   constexpr int WARPS = BLOCK / 32;
   constexpr int64_t TILE = (int64_t)BLOCK * ITEMS;
