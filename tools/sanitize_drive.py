@@ -61,4 +61,19 @@ for n in (1, 7, 33, 1000, 4099, 70_001, 300_007):
             G.dot(xc, yc)
             G.norm2sq(xc)
     torch.cuda.synchronize()
+
+# multi-group reduction finishes (grids of 129 and 300 blocks: group leaders
+# waiting on tagged slots, the grid leader folding group slots), 4-, 8- and
+# 16-byte partials on one workspace
+for n in (129 * 16384 - 3, 300 * 16384 + 5):
+    for dt in (torch.float32, torch.float64, torch.int32, torch.int64):
+        x, y = arr(n, dt), arr(n, dt)
+        G.sum(x)
+        G.max(x)
+        G.dot(x, y)
+    xc = torch.randn(n, dtype=torch.complex128, device=dev)
+    G.vdot(xc, xc)
+    G.cg_update(arr(n, torch.float32), arr(n, torch.float32), arr(n, torch.float32), arr(n, torch.float32),
+                alpha_num=torch.ones(1, device=dev), alpha_den=torch.ones(1, device=dev))
+    torch.cuda.synchronize()
 print("drive ok", G.launch_count(), "launches")

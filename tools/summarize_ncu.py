@@ -14,6 +14,7 @@ import subprocess
 import sys
 from collections import defaultdict
 
+OPS = ("axpbyz", "dot", "sum", "norm2", "scan")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROF = os.path.join(ROOT, "profiles")
 
@@ -85,23 +86,36 @@ def main():
         rows = list(csv.reader(io.StringIO(text[start:])))
         h = rows[0]
         ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-        tot = defaultdict(float)
-        cnt = defaultdict(int)
+        # bench.py launches, in order: the input fills, W + K steps of the five
+        # hot-path ops, then the e2e pipeline (2^24-element chunks).  The step
+        # table keeps the first STEP_LAUNCHES launches of each op (3 warm-up +
+        # 3 timed steps of `--steps 3 --warmup 3`); the e2e launches follow.
+        STEP_LAUNCHES = 6
+        tables = {"step": (defaultdict(float), defaultdict(int)), "all": (defaultdict(float), defaultdict(int))}
         for r in rows[1:]:
             if len(r) <= vi:
                 continue
             v = float(r[vi].replace(",", "")) * {"ns": 1e-3, "us": 1, "ms": 1e3}.get(r[ui], 1)
             op = op_of(r[ki])
-            tot[op] += v
-            cnt[op] += 1
-        all_t = sum(tot.values())
+            for name, (tot, cnt) in tables.items():
+                if name == "step" and (op not in OPS or tables["step"][1][op] >= STEP_LAUNCHES):
+                    continue
+                tot[op] += v
+                cnt[op] += 1
         out = [f"# {tag}: launch list of `bench.py --steps 3 --warmup 3` under "
                "`ncu --metrics gpu__time_duration.sum --clock-control none`", "",
-               "Cold-cache, serialised per-launch times: the SHARE column is what must agree with bench.py's "
-               "per-op split (ops.*.ms).", "", "| kernel (op) | launches | total us | mean us | share |", "|---|---|---|---|---|"]
-        for op in sorted(tot, key=lambda o: -tot[o]):
-            out.append(f"| {op} | {cnt[op]} | {tot[op]:.1f} | {tot[op] / cnt[op]:.1f} | {tot[op] / all_t * 100:.1f}% |")
-        open(os.path.join(PROF, f"{tag}_launches.md"), "w").write("\n".join(out) + "\n")
+               "Cold-cache, serialised per-launch times: the SHARE column of the step table is what must agree "
+               "with bench.py's per-op split (ops.*.ms).", ""]
+        for name, title in (("step", "Bench step (first 6 launches of each op: 3 warm-up + 3 timed steps, n = 2^28)"),
+                            ("all", "Every launch of the command (incl. the input fills and the e2e pipeline's "
+                                    "2^24-element chunks)")):
+            tot, cnt = tables[name]
+            all_t = sum(tot.values())
+            out += [f"## {title}", "", "| kernel (op) | launches | total us | mean us | share |", "|---|---|---|---|---|"]
+            for op in sorted(tot, key=lambda o: -tot[o]):
+                out.append(f"| {op} | {cnt[op]} | {tot[op]:.1f} | {tot[op] / cnt[op]:.1f} | {tot[op] / all_t * 100:.1f}% |")
+            out.append("")
+        open(os.path.join(PROF, f"{tag}_launches.md"), "w").write("\n".join(out))
 
 
 if __name__ == "__main__":
