@@ -35,7 +35,15 @@ static int run(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   X(16, int32_t, 12, 16, 8, 8, 8)   \
   X(22, int64_t, 12, 32, 8, 4, 8)   \
   X(23, int64_t, 12, 64, 8, 4, 8)   \
-  X(24, int64_t, 8, 32, 8, 4, 8)
+  X(24, int64_t, 8, 32, 8, 4, 8)    \
+  X(7, int32_t, 32, 8, 8, 8, 8)     \
+  X(8, int32_t, 8, 8, 8, 8, 8)      \
+  X(9, int32_t, 8, 16, 8, 8, 8)     \
+  X(25, int64_t, 32, 8, 4, 4, 8)    \
+  X(26, int64_t, 16, 8, 4, 4, 8)    \
+  X(27, int64_t, 12, 32, 4, 4, 8)   \
+  X(28, int64_t, 8, 48, 4, 4, 8)    \
+  X(29, int64_t, 8, 32, 4, 4, 8)
 
 extern "C" int lab_scan(int v, int64_t n, const void *in, void *out, void *ws, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
