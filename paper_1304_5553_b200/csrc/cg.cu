@@ -41,7 +41,7 @@ using namespace cg_detail;
 // Tuned shape (tools/lab/run_cg_lab.py, profiles/r1_cg.md): one 32-byte
 // vector per array per thread and pass, >= 4 CTAs per SM (64 registers), and
 // each CTA making up to 4 passes (fewer CTAs => fewer block folds and
-// last-block tickets): direction 6.1-6.3 TB/s, update 6.8 TB/s at 2^26 fp32.
+// finish slots): direction 6.1-6.3 TB/s, update 6.8 TB/s at 2^26 fp32.
 constexpr int DIR_UNROLL = 1, DIR_MINB = 4, UPD_UNROLL = 1, UPD_MINB = 4, MAX_PASSES = 4;
 
 template <typename T>

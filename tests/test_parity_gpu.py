@@ -262,7 +262,7 @@ def test_reduce_deterministic_and_reusable():
     y = synth.device_fill(synth.F32_S11, 2, n, device=DEV)
     vals = {float(ga.dot(x, y).item()) for _ in range(5)}
     assert len(vals) == 1
-    # different sizes back to back reuse the same workspace (ticket self-resets)
+    # different sizes back to back reuse the same workspace (epoch-tagged slots)
     for m in (5, 1 << 20, 3, n):
         xs = x[:m]
         xh = synth.host_fill(synth.F32_S11, 1, m)

@@ -21,12 +21,12 @@ def main():
     L = ctypes.CDLL(LIB)
     L.copy_lab.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     dev = torch.device("cuda:0")
-    a = torch.ones(1 << 30, dtype=torch.int32, device=dev)
-    b = torch.empty_like(a)
+    a = torch.ones(2 << 30, dtype=torch.int32, device=dev)  # mix21 reads a[:n] and a[n:2n]
+    b = torch.empty(1 << 30, dtype=torch.int32, device=dev)
     s = torch.cuda.current_stream().cuda_stream
     for lg in (28, 30):
         nbytes = 4 << lg
-        for v in (0, 1, 2, 3, 4, 5, 10, 11, 99):
+        for v in (0, 1, 2, 3, 4, 5, 10, 11, 20, 21, 22, 23, 99):
             def call():
                 if v == 99:
                     b[: nbytes // 4].copy_(a[: nbytes // 4])
@@ -42,7 +42,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) / reps * 1e3
-            traffic = nbytes * (1 if v in (10, 11) else 2)
+            traffic = nbytes * (1 if v in (10, 11) else 3 if v >= 20 and v < 99 else 2)
             print(f"2^{lg} int32  variant {v:2d}  {us:8.1f} us  {traffic / us / 1e3:7.1f} GB/s", flush=True)
 
 
