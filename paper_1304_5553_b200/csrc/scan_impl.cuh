@@ -29,7 +29,13 @@ using namespace scan_detail;
 // scans 10-14% faster at 2^28-2^30 and int64 inclusive 3% faster than with
 // 8 rows and spills (tools/lab/ab_scan.py); the look-back
 // reads 8 (4 for 8-byte T) predecessors per lane per round trip; warps 1..
-// load and locally scan their first phase-3 rows while warp 0 looks back.
+// load and locally scan their first phase-3 rows while warp 0 looks back,
+// and (L shape) every warp has the TMA unit prefetch its slice of the tile
+// 2/7 of a wave ahead (42 ids on 148 SMs) into L2, so the HBM reads of a
+// later tile's phase 1 fill the time this SM would otherwise idle in the
+// look-back: int32 2^28 415 -> 379 us, 2^30 1540 -> 1398 us (6.1 TB/s), int64
+// 2^28 849 -> 802 us (tools/lab/run_tile_lab.py PFV variants,
+// profiles/r1_scan_limits.md).
 // RG: the register-tile fallback for arrays that are not 16-byte aligned
 // (32-byte for a widened output): 256 threads x 16 scalar-loaded items.
 enum Shape { SHAPE_S = 0, SHAPE_M = 1, SHAPE_L = 2, SHAPE_RG = 3 };
@@ -79,10 +85,15 @@ ga_status_t run(int64_t n, const void *in, void *out, const void *carry, int64_t
     // exclusive int64 at the L shape fits 8 rows without spilling (and is 3% faster with them)
     constexpr bool ROWS8 = sizeof(T) == 4 || (EXCLUSIVE && SHAPE == SHAPE_L && std::is_integral<T>::value);
     constexpr int U = sizeof(T) != sizeof(Tin) ? UNROLLW : ROWS8 ? UNROLL4 : UNROLL8;
+    // L shape: while a tile looks back, its CTA has the TMA unit prefetch the
+    // whole input of the tile ~2/7 of a wave ahead into L2 (see the kernel)
+    // (not for widened scans: their 2x larger output changes the timing; measured 1-7% slower)
+    constexpr int PF = (SHAPE == SHAPE_L && sizeof(T) == sizeof(Tin)) ? R : 0;
+    if (PF) p.pf_dist = std::max<int64_t>(1, (int64_t)sm_count() * 2 / 7);
     if (in == out)
-      scan_l2_kernel<OP, T, Tin, W, R, U, D, false, EXCLUSIVE, true, P1U><<<grid, W * 32, 0, s>>>(p);
+      scan_l2_kernel<OP, T, Tin, W, R, U, D, false, EXCLUSIVE, true, P1U, PF><<<grid, W * 32, 0, s>>>(p);
     else
-      scan_l2_kernel<OP, T, Tin, W, R, U, D, true, EXCLUSIVE, true, P1U><<<grid, W * 32, 0, s>>>(p);
+      scan_l2_kernel<OP, T, Tin, W, R, U, D, true, EXCLUSIVE, true, P1U, PF><<<grid, W * 32, 0, s>>>(p);
   }
   count_launch();
   return check_launch("scan_kernel");

@@ -112,6 +112,7 @@ struct ScanArgs {
   int64_t carry_count;
   unsigned long long *ticket;  // {epoch:32 | counter:32}
   Status<T> status;
+  int64_t pf_dist;  // PF_ROWS kernels: prefetch into L2 the tile this many ids ahead (0: off)
 };
 
 // Spin until predecessor `idx` has published.  A predecessor that stays
@@ -325,7 +326,7 @@ __device__ __forceinline__ void draw_tile(const A &p, uint32_t &tile, uint32_t &
 // P1U: rows in flight per warp in phase 1 (its only live state is the raw
 // rows, so it can exceed phase 3's UNROLL).
 template <int OP, typename T, typename Tin, int WARPS, int ROWS, int UNROLL, int DEPTH, bool NC, bool EXCLUSIVE,
-          bool EARLY, int P1U = UNROLL>
+          bool EARLY, int P1U = UNROLL, int PF_ROWS = 0>
 __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p) {
   using O = Op<OP, T>;
   constexpr int E = Chunk<Tin>::E;  // elements per lane per row
@@ -390,6 +391,22 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p)
   acc = warp_fold<OP, T>(acc);
   if (lane == 0) s_slice[warp] = acc;
   __syncthreads();
+
+  // While warp 0 looks back (the SM has no HBM reads in flight then), every
+  // warp asks the TMA unit to pull the first PF_ROWS rows of its slice of the
+  // tile pf_dist ids ahead into L2 (cp.async.bulk.prefetch, evict_last): that
+  // tile's phase 1 — a fraction of a wave later, on whichever SM draws it —
+  // then runs on L2 hits, and the HBM reads move into this SM's idle time.
+  // A hint only: results never depend on it.
+  if constexpr (PF_ROWS > 0) {
+    const int64_t nt = tile + p.pf_dist;
+    if (p.pf_dist > 0 && lane == 0 && (nt + 1) * TILE <= p.n) {
+      const Tin *a = p.in + nt * TILE + (int64_t)warp * ROWS * ROW;
+      asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a),
+                   "r"((uint32_t)(PF_ROWS * 512)), "l"(keep)
+                   : "memory");
+    }
+  }
 
   // phase 2: slice offsets, aggregate, look-back (warp 0)
   if (warp == 0) {
@@ -557,6 +574,7 @@ ScanArgs<T, Tin> make_args(int64_t n, int64_t tile_elems, const void *in, void *
   p.out = static_cast<T *>(out);
   p.carry = static_cast<const T *>(carry);
   p.carry_count = carry_count;
+  p.pf_dist = 0;
   char *w = static_cast<char *>(ws);
   p.ticket = reinterpret_cast<unsigned long long *>(w);
   if constexpr (sizeof(T) == 4) {

@@ -7,11 +7,13 @@
 
 using namespace ga::scan_detail;
 
-template <typename T, int W, int R, int U, int D, int P1U = U>
+// PF: rows per warp prefetched into L2 for the tile PF_DIST ids ahead.
+template <typename T, int W, int R, int U, int D, int P1U = U, int PF = 0, int PF_DIST = 148>
 static int run(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   constexpr int64_t TILE = (int64_t)W * R * 512 / sizeof(T);
   ScanArgs<T> p = make_args<T>(n, TILE, in, out, nullptr, 0, ws);
-  scan_l2_kernel<GA_OP_SUM, T, T, W, R, U, D, true, true, true, P1U><<<(int)p.num_tiles, W * 32, 0, s>>>(p);
+  p.pf_dist = PF_DIST;
+  scan_l2_kernel<GA_OP_SUM, T, T, W, R, U, D, true, true, true, P1U, PF><<<(int)p.num_tiles, W * 32, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : 100 + (int)e;
 }
@@ -45,11 +47,26 @@ static int run(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   X(28, int64_t, 8, 48, 4, 4, 8)    \
   X(29, int64_t, 8, 32, 4, 4, 8)
 
+// prefetch variants (L shape): id, T, PF rows, distance
+#define PFV(X)                        \
+  X(40, int32_t, 32, 40)              \
+  X(41, int32_t, 32, 44)              \
+  X(42, int32_t, 32, 56)              \
+  X(43, int32_t, 32, 34)              \
+  X(45, int32_t, 32, 50)              \
+  X(46, int64_t, 32, 50)              \
+  X(50, int64_t, 32, 40)              \
+  X(51, int64_t, 28, 50)              \
+  X(53, int64_t, 24, 50)
+
 extern "C" int lab_scan(int v, int64_t n, const void *in, void *out, void *ws, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
   switch (v) {
 #define C(id, T, W, R, U, D, P) case id: return run<T, W, R, U, D, P>(n, in, out, ws, s);
     V(C)
+#undef C
+#define C(id, T, PF, DIST) case id: return run<T, 24, 32, 8, sizeof(T) == 8 ? 4 : 8, 8, PF, DIST>(n, in, out, ws, s);
+    PFV(C)
 #undef C
   }
   return 2;
@@ -59,7 +76,10 @@ extern "C" int64_t lab_scan_tile(int v) {
 #define C(id, T, W, R, U, D, P) case id: return (int64_t)W * R * 512 / sizeof(T);
     V(C)
 #undef C
+#define C(id, T, PF, DIST) case id: return (int64_t)24 * 32 * 512 / sizeof(T);
+    PFV(C)
+#undef C
   }
   return 0;
 }
-extern "C" int lab_scan_elem_bytes(int v) { return v >= 20 ? 8 : 4; }
+extern "C" int lab_scan_elem_bytes(int v) { return ((v >= 20 && v < 30) || v == 46 || v >= 50) ? 8 : 4; }
