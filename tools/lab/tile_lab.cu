@@ -47,17 +47,19 @@ static int run(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   X(28, int64_t, 8, 48, 4, 4, 8)    \
   X(29, int64_t, 8, 32, 4, 4, 8)
 
-// prefetch variants (L shape): id, T, PF rows, distance
+// prefetch variants: id, T, warps, rows, PF rows, distance
 #define PFV(X)                        \
-  X(40, int32_t, 32, 40)              \
-  X(41, int32_t, 32, 44)              \
-  X(42, int32_t, 32, 56)              \
-  X(43, int32_t, 32, 34)              \
-  X(45, int32_t, 32, 50)              \
-  X(46, int64_t, 32, 50)              \
-  X(50, int64_t, 32, 40)              \
-  X(51, int64_t, 28, 50)              \
-  X(53, int64_t, 24, 50)
+  X(40, int32_t, 24, 32, 32, 42)      \
+  X(41, int32_t, 24, 16, 16, 42)      \
+  X(42, int32_t, 24, 16, 16, 84)      \
+  X(43, int32_t, 12, 32, 32, 84)      \
+  X(44, int32_t, 12, 32, 32, 60)      \
+  X(45, int32_t, 24, 48, 48, 42)      \
+  X(47, int32_t, 32, 8, 8, 42)        \
+  X(48, int32_t, 32, 8, 8, 84)        \
+  X(46, int64_t, 24, 32, 32, 42)      \
+  X(50, int64_t, 12, 32, 32, 84)      \
+  X(51, int64_t, 32, 8, 8, 42)
 
 extern "C" int lab_scan(int v, int64_t n, const void *in, void *out, void *ws, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
@@ -65,7 +67,7 @@ extern "C" int lab_scan(int v, int64_t n, const void *in, void *out, void *ws, v
 #define C(id, T, W, R, U, D, P) case id: return run<T, W, R, U, D, P>(n, in, out, ws, s);
     V(C)
 #undef C
-#define C(id, T, PF, DIST) case id: return run<T, 24, 32, 8, sizeof(T) == 8 ? 4 : 8, 8, PF, DIST>(n, in, out, ws, s);
+#define C(id, T, W, R, PF, DIST) case id: return run<T, W, R, 8, sizeof(T) == 8 ? 4 : 8, 8, PF, DIST>(n, in, out, ws, s);
     PFV(C)
 #undef C
   }
@@ -76,7 +78,7 @@ extern "C" int64_t lab_scan_tile(int v) {
 #define C(id, T, W, R, U, D, P) case id: return (int64_t)W * R * 512 / sizeof(T);
     V(C)
 #undef C
-#define C(id, T, PF, DIST) case id: return (int64_t)24 * 32 * 512 / sizeof(T);
+#define C(id, T, W, R, PF, DIST) case id: return (int64_t)W * R * 512 / sizeof(T);
     PFV(C)
 #undef C
   }
