@@ -262,7 +262,7 @@ __device__ __forceinline__ Tacc fold_slots(const char *base, int count, uint32_t
 // writes *out and advances the epoch (stream order makes it visible to the
 // next call).  With one group the second level is skipped.  Only group
 // leaders wait, and only for blocks that never wait, so progress needs more
-// co-resident blocks than groups (finish_group() guarantees it; a starved
+// co-resident blocks than groups (make_finish() guarantees it; a starved
 // wait traps after 10 s).  Every fold order depends on (grid, group) only.
 template <int OP, int BLOCK, typename Tacc>
 __device__ __forceinline__ void grid_finish(Tacc v, uint32_t tag, Tacc *smem, const Finish &f, Tacc *out,
