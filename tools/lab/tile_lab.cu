@@ -47,19 +47,18 @@ static int run(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   X(28, int64_t, 8, 48, 4, 4, 8)    \
   X(29, int64_t, 8, 32, 4, 4, 8)
 
-// prefetch variants: id, T, warps, rows, PF rows, distance
-#define PFV(X)                        \
-  X(40, int32_t, 24, 32, 32, 42)      \
-  X(41, int32_t, 24, 16, 16, 42)      \
-  X(42, int32_t, 24, 16, 16, 84)      \
-  X(43, int32_t, 12, 32, 32, 84)      \
-  X(44, int32_t, 12, 32, 32, 60)      \
-  X(45, int32_t, 24, 48, 48, 42)      \
-  X(47, int32_t, 32, 8, 8, 42)        \
-  X(48, int32_t, 32, 8, 8, 84)        \
-  X(46, int64_t, 24, 32, 32, 42)      \
-  X(50, int64_t, 12, 32, 32, 84)      \
-  X(51, int64_t, 32, 8, 8, 42)
+// prefetch variants: id, T, warps, rows, PF rows, distance, phase-3 rows (UNROLL), look-back depth, phase-1 rows (P1U)
+#define PFV(X)                                  \
+  X(40, int32_t, 24, 32, 32, 42, 8, 8, 8)         \
+  X(41, int32_t, 24, 32, 32, 42, 8, 8, 16)        \
+  X(42, int32_t, 24, 32, 32, 42, 8, 8, 4)         \
+  X(43, int32_t, 24, 32, 32, 42, 4, 8, 8)         \
+  X(44, int32_t, 24, 32, 32, 42, 8, 4, 8)         \
+  X(45, int32_t, 24, 32, 32, 42, 8, 16, 8)        \
+  X(47, int32_t, 24, 32, 32, 42, 16, 8, 16)       \
+  X(46, int64_t, 24, 32, 32, 42, 4, 4, 8)         \
+  X(50, int64_t, 24, 32, 32, 42, 4, 4, 16)        \
+  X(51, int64_t, 24, 32, 32, 42, 4, 8, 8)
 
 extern "C" int lab_scan(int v, int64_t n, const void *in, void *out, void *ws, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
@@ -67,7 +66,7 @@ extern "C" int lab_scan(int v, int64_t n, const void *in, void *out, void *ws, v
 #define C(id, T, W, R, U, D, P) case id: return run<T, W, R, U, D, P>(n, in, out, ws, s);
     V(C)
 #undef C
-#define C(id, T, W, R, PF, DIST) case id: return run<T, W, R, 8, sizeof(T) == 8 ? 4 : 8, 8, PF, DIST>(n, in, out, ws, s);
+#define C(id, T, W, R, PF, DIST, U, D, P1) case id: return run<T, W, R, U, D, P1, PF, DIST>(n, in, out, ws, s);
     PFV(C)
 #undef C
   }
@@ -78,7 +77,7 @@ extern "C" int64_t lab_scan_tile(int v) {
 #define C(id, T, W, R, U, D, P) case id: return (int64_t)W * R * 512 / sizeof(T);
     V(C)
 #undef C
-#define C(id, T, W, R, PF, DIST) case id: return (int64_t)W * R * 512 / sizeof(T);
+#define C(id, T, W, R, PF, DIST, U, D, P1) case id: return (int64_t)W * R * 512 / sizeof(T);
     PFV(C)
 #undef C
   }
