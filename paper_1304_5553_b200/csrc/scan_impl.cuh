@@ -25,9 +25,10 @@ using namespace scan_detail;
 //      a small array over the SMs.
 // Every warp keeps 8 rows of 512 bytes in flight in phase 1 (P1U) and
 // UNROLL rows in phase 3: 8 for 4-byte types and exclusive int64 at the L
-// shape, 4 for the other 8-byte scans, 2 for widened ones, which keeps every instance spill-free (ptxas -v) — widened
-// scans 10-14% faster at 2^28-2^30 and int64 inclusive 3% faster than with
-// 8 rows and spills (tools/lab/ab_scan.py); the look-back
+// shape, 4 for the other 8-byte scans, 2 for widened ones, which keeps every
+// instance spill-free (ptxas -v) — widened scans 10-14% faster at
+// 2^28-2^30 and int64 inclusive 3% faster than with 8 rows and spills
+// (tools/lab/ab_scan.py); the look-back
 // reads 8 (4 for 8-byte T) predecessors per lane per round trip; warps 1..
 // load and locally scan their first phase-3 rows while warp 0 looks back,
 // and (L shape) every warp has the TMA unit prefetch its slice of the tile
