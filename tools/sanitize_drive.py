@@ -76,4 +76,12 @@ for n in (129 * 16384 - 3, 300 * 16384 + 5):
     G.cg_update(arr(n, torch.float32), arr(n, torch.float32), arr(n, torch.float32), arr(n, torch.float32),
                 alpha_num=torch.ones(1, device=dev), alpha_den=torch.ones(1, device=dev))
     torch.cuda.synchronize()
+
+# L-shape scans (>= 256 super-tiles: the look-back L2 prefetch of the tile 42
+# ids ahead is active), in place and out of place, plus a ragged tail
+for n, dt in ((256 * 98304 + 12345, torch.int32), (256 * 49152 + 777, torch.int64)):
+    x = arr(n, dt)
+    G.scan(x)
+    G.scan(x, exclusive=True, out=x)
+    torch.cuda.synchronize()
 print("drive ok", G.launch_count(), "launches")
