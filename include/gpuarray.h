@@ -19,6 +19,11 @@
  *   gpuarray_scan                      parallel prefix sum, §3.2.6
  *       "GPU-based parallel prefix sums".
  *
+ * Sharded over GPUs (BASELINE.json north_star):
+ *   gpuarray_reduce_sharded / gpuarray_scan_sharded  one call per rank on
+ *       its contiguous shard; the cross-GPU step is an NCCL collective on the
+ *       caller's stream and communicator.
+ *
  * Beyond them: the other GPUArray operators and cumath maps
  * (gpuarray_elementwise), device-scalar coefficients (gpuarray_axpbyz_ds),
  * the fused cross-GPU finish (gpuarray_reduce_xgpu), and the CG workload's
@@ -51,7 +56,7 @@
 extern "C" {
 #endif
 
-#define GPUARRAY_ABI_VERSION 4
+#define GPUARRAY_ABI_VERSION 5
 
 /* C64 / C128: complex numbers as interleaved (re, im) float / double pairs
  * ("seamless support for complex numbers"; §8(f) NEXT-3). */
@@ -75,7 +80,8 @@ typedef enum {
                                   y missing for MAP_MUL, partial overlap of output and input */
   GA_ERR_UNSUPPORTED = 2,      /* combination not instantiated (e.g. MAX with out_dt != in_dt) */
   GA_ERR_WORKSPACE = 3,        /* workspace NULL or smaller than *_workspace_bytes() */
-  GA_ERR_CUDA = 4              /* CUDA error at launch; see gpuarray_last_error() */
+  GA_ERR_CUDA = 4,             /* CUDA error at launch; see gpuarray_last_error() */
+  GA_ERR_NCCL = 5              /* NCCL missing or a collective failed to enqueue (sharded calls) */
 } ga_status_t;
 
 /* A host scalar typed like the arrays it combines with ("numpy sized
@@ -224,6 +230,49 @@ size_t gpuarray_scan_workspace_bytes(ga_dtype_t dt, int64_t n);
 ga_status_t gpuarray_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
                           const void *in, void *out, const void *carry, int64_t carry_count, void *workspace,
                           size_t workspace_bytes, void *stream);
+
+/* ---- Sharded over GPUs (BASELINE.json
+ * north_star: "Arrays are sharded contiguously ... Reductions combine per-GPU
+ * partials with one NCCL allreduce over NVLink.  Scan uses an exclusive scan
+ * of per-GPU totals followed by a local offset add").  One call per rank, on
+ * the rank's contiguous shard [start_g, start_g + n) of the global array
+ * (start_g = floor(g*N/G), R16), with every rank making the same
+ * sequence of sharded calls (collective semantics).
+ *   nccl_comm  an initialised ncclComm_t (e.g. torch's
+ *              ProcessGroupNCCL._comm_ptr()), whose rank order is the shard
+ *              order; NCCL is bound at run time from the libnccl.so.2 already
+ *              loaded in the process (else loaded; $GPUARRAY_NCCL_LIB).  A
+ *              missing NCCL or a failed enqueue returns GA_ERR_NCCL.
+ * The collective runs on `stream` after the local kernel; nothing is
+ * synchronised.  Results are identical on every rank. */
+
+/* gpuarray_reduce over the global array: the local single-pass reduction of
+ * the shard into *out (every argument as gpuarray_reduce; `workspace` is a
+ * gpuarray_reduce workspace), then ONE ncclAllReduce(out, out, 1 value, op)
+ * in place (SUM / MAX / MIN; complex: SUM of the 2 components).  Float SUM:
+ * the local tree sum, then NCCL's fixed-topology combine (R17). */
+ga_status_t gpuarray_reduce_sharded(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
+                                    const void *x, const void *y, void *out, void *workspace, size_t workspace_bytes,
+                                    void *nccl_comm, void *stream);
+
+/* Bytes of the gpuarray_scan_sharded workspace for a shard of n elements of
+ * out_dt (a reduce workspace, room for the gathered totals of up to 4096
+ * ranks, and a scan workspace).  Zero-fill once; reusable afterwards. */
+size_t gpuarray_scan_sharded_workspace_bytes(ga_dtype_t out_dt, int64_t n);
+
+/* gpuarray_scan over the global array: on rank g,
+ *   1. T_g = the fold of the shard with op (one reduce kernel, in out_dt);
+ *   2. ncclAllGather of T_0 .. T_{G-1};
+ *   3. the local scan of the shard with carry-in c ⊕ T_0 ⊕ ... ⊕ T_{g-1}, c
+ *      the fold of carry[0..carry_count) (neutral if none; one more reduce
+ *      kernel when carry_count > 0), folded into the scan kernel's tile 0.
+ * So out holds elements [start_g, start_g + n) of the scan of the global
+ * array (R18: the shard is read twice and written once).  Every
+ * argument as gpuarray_scan; widening MAX/MIN scans are GA_ERR_UNSUPPORTED.
+ * n may be 0 on some ranks (they still take part in the collective). */
+ga_status_t gpuarray_scan_sharded(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t in_dt, ga_dtype_t out_dt, int64_t n,
+                                  const void *in, void *out, const void *carry, int64_t carry_count, void *workspace,
+                                  size_t workspace_bytes, void *nccl_comm, void *stream);
 
 /* ---- Operator of the CG workload (the paper's
  * "conjugate-gradient-based Krylov solver", applied

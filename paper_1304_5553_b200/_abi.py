@@ -15,7 +15,7 @@ GA_F32, GA_F64, GA_I32, GA_I64, GA_C64, GA_C128 = 0, 1, 2, 3, 4, 5
 GA_OP_SUM, GA_OP_MAX, GA_OP_MIN = 0, 1, 2
 GA_MAP_ID, GA_MAP_MUL, GA_MAP_SQUARE, GA_MAP_CONJ_MUL = 0, 1, 2, 3
 GA_SCAN_INCLUSIVE, GA_SCAN_EXCLUSIVE = 0, 1
-GA_OK, GA_ERR_INVALID_ARGUMENT, GA_ERR_UNSUPPORTED, GA_ERR_WORKSPACE, GA_ERR_CUDA = 0, 1, 2, 3, 4
+GA_OK, GA_ERR_INVALID_ARGUMENT, GA_ERR_UNSUPPORTED, GA_ERR_WORKSPACE, GA_ERR_CUDA, GA_ERR_NCCL = 0, 1, 2, 3, 4, 5
 
 # Every symbol include/gpuarray.h declares (checked by tests/test_abi.py).
 EXPORTS = (
@@ -23,7 +23,8 @@ EXPORTS = (
     "gpuarray_scan_workspace_bytes", "gpuarray_scan", "gpuarray_status_string", "gpuarray_last_error",
     "gpuarray_abi_version", "gpuarray_launch_count", "gpuarray_xgpu_buffer_bytes", "gpuarray_reduce_xgpu",
     "gpuarray_stencil3", "gpuarray_axpbyz_ds", "gpuarray_elementwise", "gpuarray_cg_direction",
-    "gpuarray_cg_update",
+    "gpuarray_cg_update", "gpuarray_reduce_sharded", "gpuarray_scan_sharded_workspace_bytes",
+    "gpuarray_scan_sharded",
 )
 
 
@@ -123,6 +124,12 @@ def _load():
     lib.gpuarray_cg_direction.restype = st
     lib.gpuarray_cg_direction.argtypes = [st, i64, ga_dscalar_t, vp, vp, vp, ga_scalar_t, ga_scalar_t, ga_scalar_t, vp,
                                           vp, vp, vp, sz, vp]
+    lib.gpuarray_reduce_sharded.restype = st
+    lib.gpuarray_reduce_sharded.argtypes = [st, st, st, st, i64, vp, vp, vp, vp, sz, vp, vp]
+    lib.gpuarray_scan_sharded_workspace_bytes.restype = sz
+    lib.gpuarray_scan_sharded_workspace_bytes.argtypes = [st, i64]
+    lib.gpuarray_scan_sharded.restype = st
+    lib.gpuarray_scan_sharded.argtypes = [st, st, st, st, i64, vp, vp, vp, i64, vp, sz, vp, vp]
     lib.gpuarray_cg_update.restype = st
     lib.gpuarray_cg_update.argtypes = [st, i64, ga_dscalar_t, vp, vp, vp, vp, vp, vp, sz, vp]
     return lib
@@ -171,6 +178,21 @@ def gpuarray_scan_workspace_bytes(dt, n):
 def gpuarray_scan(op, kind, in_dt, out_dt, n, in_, out, carry, carry_count, workspace, workspace_bytes, stream):
     return LIB.gpuarray_scan(op, kind, in_dt, out_dt, n, in_, out, carry, carry_count, workspace, workspace_bytes,
                              stream)
+
+
+def gpuarray_reduce_sharded(op, map_, in_dt, out_dt, n, x, y, out, workspace, workspace_bytes, nccl_comm, stream):
+    return LIB.gpuarray_reduce_sharded(op, map_, in_dt, out_dt, n, x, y, out, workspace, workspace_bytes, nccl_comm,
+                                       stream)
+
+
+def gpuarray_scan_sharded_workspace_bytes(out_dt, n):
+    return LIB.gpuarray_scan_sharded_workspace_bytes(out_dt, n)
+
+
+def gpuarray_scan_sharded(op, kind, in_dt, out_dt, n, in_, out, carry, carry_count, workspace, workspace_bytes,
+                          nccl_comm, stream):
+    return LIB.gpuarray_scan_sharded(op, kind, in_dt, out_dt, n, in_, out, carry, carry_count, workspace,
+                                     workspace_bytes, nccl_comm, stream)
 
 
 GA_EW_MUL, GA_EW_DIV, GA_EW_SQRT, GA_EW_ABS, GA_EW_NEG, GA_EW_EXP, GA_EW_LOG, GA_EW_SIN, GA_EW_COS, GA_EW_MAX, \

@@ -28,6 +28,14 @@ NVCC_FLAGS = [
 ]
 
 
+def nccl_include():
+    """nccl.h for the sharded entry points (types only: NCCL is bound at run
+    time with dlopen).  The NCCL wheel torch links against, else the system's."""
+    import sysconfig
+    cand = os.path.join(sysconfig.get_paths()["purelib"], "nvidia", "nccl", "include")
+    return cand if os.path.exists(os.path.join(cand, "nccl.h")) else "/usr/include"
+
+
 def nvcc():
     cand = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "bin", "nvcc")
     return cand if os.path.exists(cand) else "nvcc"
@@ -51,14 +59,15 @@ def build(force=False, verbose=False):
     jobs = []
     for src in SOURCES:
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        jobs.append((obj, [nvcc(), *compile_flags, "-I", os.path.join(ROOT, "include"), "-c", "-o", obj, src]))
+        jobs.append((obj, [nvcc(), *compile_flags, "-I", os.path.join(ROOT, "include"), "-I", nccl_include(),
+                           "-c", "-o", obj, src]))
     with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
         for obj, cmd in jobs:
             if verbose:
                 print(" ".join(cmd), flush=True)
         list(ex.map(lambda j: subprocess.check_call(j[1]), jobs))
     link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
-            "-o", LIB + ".tmp", *[o for o, _ in jobs]]
+            "-o", LIB + ".tmp", *[o for o, _ in jobs], "-ldl"]
     subprocess.check_call(link)
     os.replace(LIB + ".tmp", LIB)
     return LIB

@@ -274,6 +274,7 @@ const char *gpuarray_status_string(ga_status_t s) {
     case GA_ERR_UNSUPPORTED: return "GA_ERR_UNSUPPORTED";
     case GA_ERR_WORKSPACE: return "GA_ERR_WORKSPACE";
     case GA_ERR_CUDA: return "GA_ERR_CUDA";
+    case GA_ERR_NCCL: return "GA_ERR_NCCL";
   }
   return "GA_ERR_UNKNOWN";
 }

@@ -19,12 +19,16 @@
 //   - phase 3 re-reads the slice (L2 hit, evict_first), scans it row by row
 //     (in-chunk serial scan + warp shuffle scan) and stores 512 B per warp
 //     instruction.
-// Look-back status words carry the call's epoch, so the workspace is zeroed
-// once and never again; the CTA drawing the last id resets the counter.
+// Look-back status words carry the call's epoch in every 64-bit word (for
+// every element size, so one workspace may serve scans of any dtype, size and
+// shape), so the workspace is zeroed once and never again (until the 30-bit
+// epoch wraps: see gpuarray_scan_workspace_bytes); the CTA drawing the last
+// id resets the counter.
 // Tile 0's exclusive prefix is the carry-in c = sum(carry[0..carry_count)),
 // which is how a sharded scan injects the totals of earlier shards.
-// tools/lab/scan_lab.cu keeps the alternatives that were measured against
-// this one (register-tiled single-touch, TMA-staged, warp-specialized).
+// The alternatives measured against this one (register-tiled single-touch,
+// TMA-staged, warp-specialized, persistent look-ahead) are summarised in
+// DESIGN.md §6 and profiles/r1_scan_limits.md.
 #include <cuda_runtime.h>
 #include <stdint.h>
 

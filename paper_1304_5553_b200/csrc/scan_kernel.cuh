@@ -10,7 +10,7 @@
 //   scan_reg_kernel the fallback for arrays that are not 16-byte aligned:
 //                   one register tile per CTA, scalar loads.
 // Both share the decoupled look-back machinery below.  The alternatives
-// measured while tuning are kept, frozen, in tools/lab/scan_variants.cuh.
+// measured while tuning are described in DESIGN.md §6 (tuning history).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -26,11 +26,6 @@ constexpr uint32_t EPOCH_MASK = (1u << 30) - 1;
 // own 256-byte block; per-tile status follows.
 constexpr size_t HEADER = 256;
 
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
   uint64_t v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -38,9 +33,6 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
 }
 __device__ __forceinline__ void st_relaxed_u64(uint64_t *p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
@@ -59,44 +51,70 @@ __device__ __forceinline__ T from_bits32(uint32_t b) {
   if constexpr (std::is_same<T, float>::value) return __uint_as_float(b);
   else return (T)b;
 }
+// 64-bit payload of an 8-byte element.
+template <typename T>
+__device__ __forceinline__ uint64_t to_bits64(T v) {
+  if constexpr (std::is_same<T, double>::value) return (uint64_t)__double_as_longlong(v);
+  else return (uint64_t)v;
+}
+template <typename T>
+__device__ __forceinline__ T from_bits64(uint64_t b) {
+  if constexpr (std::is_same<T, double>::value) return __longlong_as_double((long long)b);
+  else return (T)b;
+}
 
-// Look-back status of one tile.
-//  4-byte T: one 64-bit word  (epoch:30 | flag:2) << 32 | bits(value) — flag
-//            and value are written and read together (single-copy atomic).
-//  8-byte T: a 32-bit flag word (epoch:30 | flag:2) released after the value
-//            is stored in agg[] or incl[]; readers acquire the flag first.
+// Look-back status of one tile.  Every 64-bit word of the status region
+// carries a tag (epoch:30 | flag:2) in its high half and 32 payload bits in
+// its low half, whatever the element size, at a per-tile stride of
+// sizeof(T) * 2 bytes from the same base:
+//  4-byte T: one word   tag << 32 | bits(value);
+//  8-byte T: two words  tag << 32 | lo32(value),  tag << 32 | hi32(value).
+// Each word is written and read with single-copy-atomic 64-bit accesses; a
+// status is valid for the current call when every word carries the call's
+// epoch and the same flag (an 8-byte status caught between its AGGREGATE
+// and INCLUSIVE publications shows two flags and is re-read).  Because the
+// region never holds an untagged word, a workspace reused across element
+// sizes, tile counts and shapes can only show tags of earlier epochs, which
+// never match (the layout-independent status).
 template <typename T, int SZ = sizeof(T)>
 struct Status;
+
+__device__ __forceinline__ uint64_t tag_word(uint32_t epoch, uint32_t flag, uint32_t payload) {
+  return ((uint64_t)((epoch << 2) | flag) << 32) | payload;
+}
+__device__ __forceinline__ uint32_t tag_flag(uint32_t hi, uint32_t epoch) {
+  return (hi >> 2) == epoch ? (hi & 3u) : FLAG_INVALID;
+}
 
 template <typename T>
 struct Status<T, 4> {
   uint64_t *word;
   __device__ void publish(int64_t tile, uint32_t epoch, uint32_t flag, T v) const {
-    st_relaxed_u64(word + tile, ((uint64_t)((epoch << 2) | flag) << 32) | to_bits32<T>(v));
+    st_relaxed_u64(word + tile, tag_word(epoch, flag, to_bits32<T>(v)));
   }
   __device__ uint32_t read(int64_t tile, uint32_t epoch, T &v) const {
     const uint64_t w = ld_relaxed_u64(word + tile);
-    const uint32_t hi = (uint32_t)(w >> 32);
     v = from_bits32<T>((uint32_t)w);
-    return (hi >> 2) == epoch ? (hi & 3u) : FLAG_INVALID;
+    return tag_flag((uint32_t)(w >> 32), epoch);
   }
 };
 
 template <typename T>
 struct Status<T, 8> {
-  uint32_t *flag;
-  T *agg;
-  T *incl;
-  __device__ void publish(int64_t tile, uint32_t epoch, uint32_t f, T v) const {
-    (f == FLAG_INCLUSIVE ? incl : agg)[tile] = v;
-    st_release_u32(flag + tile, (epoch << 2) | f);
+  uint64_t *word;  // two words per tile
+  __device__ void publish(int64_t tile, uint32_t epoch, uint32_t flag, T v) const {
+    const uint64_t b = to_bits64<T>(v);
+    const uint64_t lo = tag_word(epoch, flag, (uint32_t)b), hi = tag_word(epoch, flag, (uint32_t)(b >> 32));
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(word + 2 * tile), "l"(lo), "l"(hi)
+                 : "memory");
   }
   __device__ uint32_t read(int64_t tile, uint32_t epoch, T &v) const {
-    const uint32_t w = ld_acquire_u32(flag + tile);
-    const uint32_t f = (w >> 2) == epoch ? (w & 3u) : FLAG_INVALID;
-    if (f == FLAG_AGGREGATE) v = __ldcg(agg + tile);
-    else if (f == FLAG_INCLUSIVE) v = __ldcg(incl + tile);
-    return f;
+    uint64_t lo, hi;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(word + 2 * tile)
+                 : "memory");
+    const uint32_t tlo = (uint32_t)(lo >> 32), thi = (uint32_t)(hi >> 32);
+    v = from_bits64<T>(((uint64_t)(uint32_t)hi << 32) | (uint32_t)lo);
+    return tlo == thi ? tag_flag(tlo, epoch) : FLAG_INVALID;
   }
 };
 
@@ -140,7 +158,7 @@ __device__ __forceinline__ uint32_t wait_status(const Status<T> &st, int64_t idx
 // max/min results are exact; float SUM depends on which predecessors were
 // INCLUSIVE at the time (R22).
 template <int OP, typename T, int DEPTH>
-__device__ T look_back(const Status<T> &st, int64_t tile, uint32_t epoch) {
+__device__ __noinline__ T look_back(const Status<T> &st, int64_t tile, uint32_t epoch) {
   const int lane = threadIdx.x & 31;
   const T neutral = Op<OP, T>::neutral();
   T prefix = neutral;
@@ -559,8 +577,7 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_reg_kernel(ScanArgs<T, Tin> p) 
 
 template <typename T>
 size_t status_bytes(int64_t tiles) {
-  if (sizeof(T) == 4) return (size_t)tiles * 8;
-  return (size_t)((tiles * 4 + 15) / 16) * 16 + (size_t)tiles * 16;
+  return (size_t)tiles * 2 * sizeof(T);  // 8 (4-byte T) or 16 (8-byte T) tagged bytes per tile
 }
 
 // Fill the argument block for a tile size of tile_elems elements.
@@ -577,14 +594,7 @@ ScanArgs<T, Tin> make_args(int64_t n, int64_t tile_elems, const void *in, void *
   p.pf_dist = 0;
   char *w = static_cast<char *>(ws);
   p.ticket = reinterpret_cast<unsigned long long *>(w);
-  if constexpr (sizeof(T) == 4) {
-    p.status.word = reinterpret_cast<uint64_t *>(w + HEADER);
-  } else {
-    p.status.flag = reinterpret_cast<uint32_t *>(w + HEADER);
-    char *vals = w + HEADER + ((p.num_tiles * 4 + 15) / 16) * 16;
-    p.status.agg = reinterpret_cast<T *>(vals);
-    p.status.incl = reinterpret_cast<T *>(vals + p.num_tiles * 8);
-  }
+  p.status.word = reinterpret_cast<uint64_t *>(w + HEADER);  // same base for every T (see Status)
   return p;
 }
 

@@ -78,21 +78,32 @@ def _ptr(t):
 # --------------------------------------------------------------- workspaces
 # One zero-filled workspace per (kernel family, device, stream); the kernels
 # keep it valid across calls (epoch-tagged reduce slots / epoch-tagged scan
-# status), so it is zeroed once at allocation and never again.  Reduce and
-# scan workspaces have different layouts and are never shared.
+# status), so it is zeroed at allocation and then only when its epoch could
+# wrap: the scan epoch has 30 bits and the reduce tag 31, so a workspace is
+# re-zeroed (on the call's stream, stream-ordered) every WRAP_CALLS calls,
+# long before a stale word could match a recycled epoch.  Reduce and scan
+# workspaces have different layouts and are never shared; scan workspaces are
+# also kept apart by element size (the status layout is tagged word by word
+# for every size, so sharing would be correct too — tests/
+# test_scan_workspace_gpu.py shares one on purpose).
+WRAP_CALLS = 1 << 29
 _ws = {}
 
 
 def workspace(kind, device, stream, nbytes):
     key = (kind, device.index, stream)
-    w = _ws.get(key)
-    if w is None or w.numel() < nbytes:
+    e = _ws.get(key)
+    if e is None or e[0].numel() < nbytes:
         size = builtins.max(nbytes, 1 << 16)
-        if w is not None:
-            size = builtins.max(size, 2 * w.numel())
-        w = torch.zeros(size, dtype=torch.uint8, device=device)
-        _ws[key] = w
-    return w
+        if e is not None:
+            size = builtins.max(size, 2 * e[0].numel())
+        e = [torch.zeros(size, dtype=torch.uint8, device=device), 0]
+        _ws[key] = e
+    e[1] += 1
+    if e[1] >= WRAP_CALLS:
+        e[0].zero_()  # torch's current stream on this device == the call's stream
+        e[1] = 1
+    return e[0]
 
 
 # --------------------------------------------------------------- elementwise
@@ -367,7 +378,7 @@ def scan(x, exclusive=False, out=None, carry=None, op=SUM, out_dtype=None):
         cptr, ccount = None, 0
     s = _stream(x)
     nb = _abi.gpuarray_scan_workspace_bytes(dt, x.numel())
-    w = workspace("scan", x.device, s, nb)
+    w = workspace(f"scan{x.element_size() if out_dtype == x.dtype else 8}", x.device, s, nb)
     kind = GA_SCAN_EXCLUSIVE if exclusive else GA_SCAN_INCLUSIVE
     check(_abi.gpuarray_scan(op, kind, in_dt, dt, x.numel(), _ptr(x), _ptr(out), cptr, ccount, w.data_ptr(),
                              w.numel(), s))

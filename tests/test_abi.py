@@ -24,7 +24,7 @@ def abi():
 
 def test_exports_every_declared_symbol(abi):
     declared = header_symbols()
-    assert len(declared) == 17
+    assert len(declared) == 20
     assert sorted(abi.EXPORTS) == declared
     for name in declared:
         assert hasattr(abi.LIB, name), name
@@ -38,9 +38,10 @@ def test_nm_shows_c_linkage(abi):
 
 
 def test_version_and_strings(abi):
-    assert abi.gpuarray_abi_version() == 4
+    assert abi.gpuarray_abi_version() == 5
     assert abi.gpuarray_status_string(abi.GA_OK) == "GA_OK"
     assert abi.gpuarray_status_string(abi.GA_ERR_CUDA) == "GA_ERR_CUDA"
+    assert abi.gpuarray_status_string(abi.GA_ERR_NCCL) == "GA_ERR_NCCL"
     assert abi.gpuarray_status_string(99) == "GA_ERR_UNKNOWN"
 
 
@@ -51,9 +52,9 @@ def test_workspace_sizes(abi):
     assert a == 256 + 8 * ((1 << 30) // 4096)
     b = abi.gpuarray_scan_workspace_bytes(abi.GA_I64, 1 << 20)
     tiles = (1 << 20) // 4096  # status for the smaller (fallback) tile of 4096 elements
-    assert b == 256 + tiles * 4 + tiles * 16
-    assert abi.gpuarray_scan_workspace_bytes(abi.GA_F32, 100) == a * 0 + 256 + 8   # float scans too
-    assert abi.gpuarray_scan_workspace_bytes(abi.GA_F64, 4096) == 256 + 16 + 16
+    assert b == 256 + tiles * 16  # two tagged 64-bit words per tile for 8-byte types
+    assert abi.gpuarray_scan_workspace_bytes(abi.GA_F32, 100) == 256 + 8   # float scans too
+    assert abi.gpuarray_scan_workspace_bytes(abi.GA_F64, 4096) == 256 + 16
 
 
 def test_argument_validation_is_synchronous(abi):
@@ -95,6 +96,27 @@ def test_argument_validation_is_synchronous(abi):
     assert "in place" in abi.gpuarray_last_error()
     assert S(0, 0, I32, I32, 100, 4096, 8192, None, 0, 64, sw - 1, None) == abi.GA_ERR_WORKSPACE
     assert S(0, 0, I32, I32, 0, None, None, None, 0, None, 0, None) == abi.GA_OK           # n == 0 no-op
+
+
+def test_sharded_validation(abi):
+    """The sharded entries validate synchronously like the local ones; a NULL
+    communicator is an argument error (no NCCL call is made)."""
+    E = abi.GA_ERR_INVALID_ARGUMENT
+    ws = abi.gpuarray_reduce_workspace_bytes(abi.GA_F32, 4)
+    RS = abi.gpuarray_reduce_sharded
+    assert RS(0, 0, 0, 0, 4, 4096, None, 64, 128, ws, None, None) == E                       # no comm
+    assert RS(1, 0, abi.GA_C64, abi.GA_C64, 4, 4096, None, 64, 128, ws, 0x1000, None) == abi.GA_ERR_UNSUPPORTED
+    SS = abi.gpuarray_scan_sharded
+    I32, I64 = abi.GA_I32, abi.GA_I64
+    sw = abi.gpuarray_scan_sharded_workspace_bytes(I32, 100)
+    # reduce workspace + carries (4098 x 8 B, rounded to 256 B) + scan workspace
+    red = abi.gpuarray_reduce_workspace_bytes(I32, 100)
+    assert sw == (red + 4098 * 8 + 255) // 256 * 256 + abi.gpuarray_scan_workspace_bytes(I32, 100)
+    assert SS(0, 0, I32, I32, 100, 4096, 8192, None, 0, 64, sw, None, None) == E              # no comm
+    assert SS(0, 0, I32, I32, -1, 4096, 8192, None, 0, 64, sw, 0x1000, None) == E             # n < 0
+    assert SS(0, 0, I32, I32, 100, 4096, 8192, None, 3, 64, sw, 0x1000, None) == E            # carry NULL
+    assert SS(1, 0, I32, I64, 100, 4096, 8192, None, 0, 64, sw, 0x1000, None) == abi.GA_ERR_UNSUPPORTED
+    assert SS(0, 0, I32, I32, 100, 4096, 8192, None, 0, 64, sw - 1, 0x1000, None) == abi.GA_ERR_WORKSPACE
 
 
 def test_cg_step_validation(abi):

@@ -34,7 +34,7 @@ def main():
         off = int(os.environ["STEP_SCAN_WS_OFFSET"], 0)
         arena = torch.zeros(8 << 20, dtype=torch.uint8, device=dev)
         base = (-arena.data_ptr()) % (2 << 20)
-        G._ws[("scan", dev.index, torch.cuda.current_stream(dev).cuda_stream)] = arena[base + off:base + off + (1 << 20)]
+        G._ws[("scan4", dev.index, torch.cuda.current_stream(dev).cuda_stream)] = [arena[base + off:base + off + (1 << 20)], 0]
     # STEP_WS_LAYOUT=same|apart: the reduce and scan workspaces in one 2 MiB
     # page (reduce at +0x200, scan at +0x100200) or in two different pages
     lay = os.environ.get("STEP_WS_LAYOUT")
@@ -44,8 +44,8 @@ def main():
         st = torch.cuda.current_stream(dev).cuda_stream
         r_off = base + 0x200
         s_off = base + (0x100200 if lay == "same" else (6 << 20) + 0x200)
-        G._ws[("reduce", dev.index, st)] = arena[r_off:r_off + (1 << 20) + 65536]
-        G._ws[("scan", dev.index, st)] = arena[s_off:s_off + (1 << 20) - 0x400]
+        G._ws[("reduce", dev.index, st)] = [arena[r_off:r_off + (1 << 20) + 65536], 0]
+        G._ws[("scan4", dev.index, st)] = [arena[s_off:s_off + (1 << 20) - 0x400], 0]
     ops = {
         "axpbyz": lambda: G.axpbyz(5.0, x, 6.0, y, out=z),
         "dot": lambda: G.reduce(G.SUM, G.MUL, x, y, out=red[0:1]),
@@ -64,7 +64,7 @@ def main():
             if it >= 10:
                 ev[o].append((e0, e1))
     torch.cuda.synchronize()
-    wsp = {kk[0]: "%#x" % w.data_ptr() for kk, w in G._ws.items()}
+    wsp = {kk[0]: "%#x" % w[0].data_ptr() for kk, w in G._ws.items()}
     print(wsp, " ".join(f"{o}:{statistics.mean(a.elapsed_time(b) for a, b in ev[o]) * 1e3:.1f}" for o in order),
           flush=True)
 
