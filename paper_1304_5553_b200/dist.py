@@ -4,20 +4,52 @@ Arrays are sharded contiguously: rank g of G owns global indices
 [start_g, start_{g+1}) with start_g = floor(g*n/G) (R16).
 
   elementwise   shard-local, no communication
-  reductions    local single-pass reduce -> ONE scalar allreduce (NCCL over
-                NVLink via torch.distributed)
-  scan          local reduce -> allgather of the G shard totals -> local
-                single-pass scan whose carry-in is the sum of the totals of
+  reductions    local single-pass reduce -> ONE scalar NCCL allreduce
+                
+  scan          local reduce -> NCCL allgather of the G shard totals -> local
+                single-pass scan whose carry-in is the fold of the totals of
                 ranks < g: 3 element-sizes of HBM
                 traffic per element instead of the 4 of scan-then-add.
 
-torch.distributed is plumbing only (process group + NCCL collective on the
-compute stream); every step of the path that touches the arrays is a
-libgpuarray.so kernel.  `ops` can be replaced (tests pass a CPU stand-in to
-exercise this host logic under gloo); the default is the CUDA path.
+With an NCCL process group, reduce() and scan() are ONE call each into the C
+ABI (gpuarray_reduce_sharded / gpuarray_scan_sharded), which runs the local
+kernels and the NCCL collective on the caller's stream with the group's own
+communicator (ProcessGroupNCCL._comm_ptr()): torch supplies the process
+group, nothing else.  With another backend (gloo: the CPU tests of this host
+logic, or ranks sharing one GPU) the same choreography runs with the local
+operations from `ops` and the collectives from torch.distributed; `ops`
+defaults to the CUDA kernels (tests pass a CPU stand-in).
 """
 import torch
 import torch.distributed as dist
+
+_COMMS = {}
+
+
+def nccl_comm(group=None, device=None):
+    """The ncclComm_t (as an int) of `group`'s NCCL backend on `device`
+    (default: the current CUDA device), or None when the group is not NCCL.
+    A lazily created communicator is created by one tiny collective."""
+    if not dist.is_initialized():
+        return None
+    pg = group or dist.group.WORLD
+    if dist.get_backend(pg) != "nccl":
+        return None
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    key = (id(pg), device.index)
+    ptr = _COMMS.get(key)
+    if ptr:
+        return ptr
+    be = pg._get_backend(device)
+    ptr = be._comm_ptr()
+    if not ptr:
+        dist.all_reduce(torch.zeros(1, device=device), group=pg)
+        torch.cuda.synchronize(device)
+        ptr = be._comm_ptr()
+    if not ptr:
+        raise RuntimeError("NCCL process group has no communicator on this device")
+    _COMMS[key] = ptr
+    return ptr
 
 
 def shard_range(n, world, rank):
@@ -57,6 +89,10 @@ def reduce(op, map_, x, y=None, out_dtype=None, out=None, group=None, ops=None):
     """Global map-reduce of a sharded array: local reduce, then one scalar
     allreduce.  Every rank ends with the same bits (NCCL's result is
     identical on all ranks)."""
+    comm = nccl_comm(group, x.device) if ops is None and x.is_cuda else None
+    if comm is not None:
+        from . import gpuarray as G
+        return G.reduce(op, map_, x, y, out_dtype=out_dtype, out=out, nccl_comm=comm)
     ops = ops or CudaOps()
     r = ops.reduce(op, map_, x, y, out_dtype=out_dtype, out=out)
     if dist.is_initialized() and dist.get_world_size(group) > 1:
@@ -75,8 +111,14 @@ def reduce_many(specs, out, group=None, ops=None):
     return out
 
 
-def scan(x, exclusive=False, out=None, group=None, ops=None, totals=None):
-    """Global prefix sum of a sharded integer array (wrapping)."""
+def scan(x, exclusive=False, out=None, group=None, ops=None, totals=None, op=0, out_dtype=None):
+    """Global scan (SUM / MAX / MIN) of a sharded array (integers wrap)."""
+    comm = nccl_comm(group, x.device) if ops is None and x.is_cuda else None
+    if comm is not None:
+        from . import gpuarray as G
+        return G.scan(x, exclusive=exclusive, out=out, op=op, out_dtype=out_dtype, nccl_comm=comm)
+    if op != 0 or out_dtype not in (None, x.dtype):
+        raise ValueError("the torch.distributed path scans with SUM in the element type only")
     ops = ops or CudaOps()
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:

@@ -298,9 +298,12 @@ def cos(x, out=None):
 
 
 # --------------------------------------------------------------- map-reduce
-def reduce(op, map_, x, y=None, out_dtype=None, out=None):
+def reduce(op, map_, x, y=None, out_dtype=None, out=None, nccl_comm=None):
     """Fold map(x, y) with op from its neutral element; returns a 0-d device
-    tensor of out_dtype (default: x.dtype)."""
+    tensor of out_dtype (default: x.dtype).  With `nccl_comm` (an ncclComm_t
+    as an int), x is this rank's shard and the result is the fold over every
+    rank's shard (gpuarray_reduce_sharded: local kernel + one NCCL
+    allreduce on the current stream)."""
     _check_array("x", x)
     has_y = map_ in (MUL, CONJ_MUL)
     if has_y:
@@ -317,6 +320,10 @@ def reduce(op, map_, x, y=None, out_dtype=None, out=None):
     s = _stream(x)
     nb = _abi.gpuarray_reduce_workspace_bytes(out_dt, x.numel())
     w = workspace("reduce", x.device, s, nb)
+    if nccl_comm is not None:
+        check(_abi.gpuarray_reduce_sharded(op, map_, in_dt, out_dt, x.numel(), _ptr(x), _ptr(y) if has_y else None,
+                                           out.data_ptr(), w.data_ptr(), w.numel(), nccl_comm, s))
+        return out
     check(_abi.gpuarray_reduce(op, map_, in_dt, out_dt, x.numel(), _ptr(x), _ptr(y) if has_y else None,
                                out.data_ptr(), w.data_ptr(), w.numel(), s))
     return out
@@ -351,13 +358,16 @@ def min(x, out=None):  # noqa: A001
 
 
 # --------------------------------------------------------------- scan
-def scan(x, exclusive=False, out=None, carry=None, op=SUM, out_dtype=None):
+def scan(x, exclusive=False, out=None, carry=None, op=SUM, out_dtype=None, nccl_comm=None):
     """Scan with reduction expression `op` (SUM / MAX / MIN) over int32,
     int64 (wrapping), float32, float64 (PAPER.md:496-499).  `out_dtype`
     (default x.dtype) may widen int32 -> int64 or float32 -> float64: the
     scan then runs in the wide type (NEXT-2).  `carry` is an optional 1-D
     device tensor of out_dtype whose elements are all folded in front (a
-    sharded scan's offset)."""
+    sharded scan's offset).  With `nccl_comm` (an ncclComm_t as an int), x is
+    this rank's shard and out its part of the scan of the global array
+    (gpuarray_scan_sharded: local reduce, NCCL allgather of the shard
+    totals, local scan with their prefix as carry-in)."""
     _check_array("x", x)
     out_dtype = x.dtype if out_dtype is None else out_dtype
     if out is None:
@@ -377,9 +387,16 @@ def scan(x, exclusive=False, out=None, carry=None, op=SUM, out_dtype=None):
     else:
         cptr, ccount = None, 0
     s = _stream(x)
-    nb = _abi.gpuarray_scan_workspace_bytes(dt, x.numel())
-    w = workspace(f"scan{x.element_size() if out_dtype == x.dtype else 8}", x.device, s, nb)
     kind = GA_SCAN_EXCLUSIVE if exclusive else GA_SCAN_INCLUSIVE
+    esize = x.element_size() if out_dtype == x.dtype else 8
+    if nccl_comm is not None:
+        nb = _abi.gpuarray_scan_sharded_workspace_bytes(dt, x.numel())
+        w = workspace(f"scan_sharded{esize}", x.device, s, nb)
+        check(_abi.gpuarray_scan_sharded(op, kind, in_dt, dt, x.numel(), _ptr(x), _ptr(out), cptr, ccount,
+                                         w.data_ptr(), w.numel(), nccl_comm, s))
+        return out
+    nb = _abi.gpuarray_scan_workspace_bytes(dt, x.numel())
+    w = workspace(f"scan{esize}", x.device, s, nb)
     check(_abi.gpuarray_scan(op, kind, in_dt, dt, x.numel(), _ptr(x), _ptr(out), cptr, ccount, w.data_ptr(),
                              w.numel(), s))
     return out
