@@ -86,9 +86,9 @@ ga_status_t run_direction(int64_t n, const ga_dscalar_t &beta, const void *r, co
   const int grid = grid_for(n, a.nvec, DIR_UNROLL);
   a.fin = make_finish(ws, grid, DIR_MINB);
   if (diag)
-    cg_direction_kernel<T, DIR_UNROLL, DIR_MINB, true><<<grid, CG_BLOCK, 0, s>>>(a);
+    launch(cg_direction_kernel<T, DIR_UNROLL, DIR_MINB, true>, grid, CG_BLOCK, 0, s, a);
   else
-    cg_direction_kernel<T, DIR_UNROLL, DIR_MINB, false><<<grid, CG_BLOCK, 0, s>>>(a);
+    launch(cg_direction_kernel<T, DIR_UNROLL, DIR_MINB, false>, grid, CG_BLOCK, 0, s, a);
   count_launch();
   return check_launch("cg_direction_kernel");
 }
@@ -111,7 +111,7 @@ ga_status_t run_update(int64_t n, const ga_dscalar_t &alpha, void *x, void *r, c
   a.nvec = vec ? n / VEC : 0;
   const int grid = grid_for(n, a.nvec, UPD_UNROLL);
   a.fin = make_finish(ws, grid, UPD_MINB);
-  cg_update_kernel<T, UPD_UNROLL, UPD_MINB><<<grid, CG_BLOCK, 0, s>>>(a);
+  launch(cg_update_kernel<T, UPD_UNROLL, UPD_MINB>, grid, CG_BLOCK, 0, s, a);
   count_launch();
   return check_launch("cg_update_kernel");
 }

@@ -72,6 +72,7 @@ __device__ __forceinline__ T lane_tree(T (&acc)[VEC]) {
 // DIAG: a diagonal array is read (a.diag != nullptr) instead of the constant d.
 template <typename T, int CG_UNROLL, int CG_MINB, bool DIAG>
 __global__ void __launch_bounds__(CG_BLOCK, CG_MINB) cg_direction_kernel(DirArgs<T> a) {
+  pdl_enter();
   constexpr int VEC = 32 / sizeof(T);
   __shared__ T smem[CG_BLOCK / 32];
   const uint32_t tag = finish_tag(a.fin);
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(CG_BLOCK, CG_MINB) cg_direction_kernel(DirArgs
 
 template <typename T, int CG_UNROLL, int CG_MINB>
 __global__ void __launch_bounds__(CG_BLOCK, CG_MINB) cg_update_kernel(UpdArgs<T> a) {
+  pdl_enter();
   constexpr int VEC = 32 / sizeof(T);
   __shared__ T smem[CG_BLOCK / 32];
   const uint32_t tag = finish_tag(a.fin);

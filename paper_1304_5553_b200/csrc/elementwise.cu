@@ -54,6 +54,7 @@ __device__ __forceinline__ T stmt(T a, T x, T b, T y) {
 // sequence (the IEEE division behind the factors is itself FMA-based).
 template <typename T, bool HAS_Y, int UNROLL, bool NC, bool DS>
 __global__ void __launch_bounds__(EW_BLOCK) ew_vec_kernel(EwArgs<T> p) {
+  pdl_enter();
   constexpr int VEC = 32 / sizeof(T);
   const int64_t tid = (int64_t)blockIdx.x * EW_BLOCK + threadIdx.x;
   if constexpr (DS) {
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(EW_BLOCK) ew_vec_kernel(EwArgs<T> p) {
 // Arrays not co-aligned modulo 32 B: scalar grid-stride loop, still one pass.
 template <typename T, bool HAS_Y, bool DS>
 __global__ void __launch_bounds__(EW_BLOCK) ew_scalar_kernel(EwArgs<T> p) {
+  pdl_enter();
   const int64_t nthreads = (int64_t)gridDim.x * EW_BLOCK;
   if constexpr (DS) {
     p.a = coef(p.a, p.an, p.ad);
@@ -163,8 +165,8 @@ ga_status_t launch_ew(int64_t n, const ga_scalar_t &a, const void *x, const ga_s
     int grid = (int)std::min<int64_t>(cdiv(n, EW_BLOCK), max_grid);
     p.head = 0;
     p.nvec = 0;
-    if (ds) ew_scalar_kernel<T, HAS_Y, true><<<grid, EW_BLOCK, 0, s>>>(p);
-    else ew_scalar_kernel<T, HAS_Y, false><<<grid, EW_BLOCK, 0, s>>>(p);
+    if (ds) launch(ew_scalar_kernel<T, HAS_Y, true>, grid, EW_BLOCK, 0, s, p);
+    else launch(ew_scalar_kernel<T, HAS_Y, false>, grid, EW_BLOCK, 0, s, p);
     count_launch();
     return check_launch("ew_scalar_kernel");
   }
@@ -175,11 +177,11 @@ ga_status_t launch_ew(int64_t n, const ga_scalar_t &a, const void *x, const ga_s
   const bool inplace = z == x || (HAS_Y && z == y);
   int grid = (int)std::min<int64_t>(std::max<int64_t>(cdiv(p.nvec, CHUNK), 1), 0x7fffffffLL);
   if (ds) {
-    if (inplace) ew_vec_kernel<T, HAS_Y, UNROLL, false, true><<<grid, EW_BLOCK, 0, s>>>(p);
-    else ew_vec_kernel<T, HAS_Y, UNROLL, true, true><<<grid, EW_BLOCK, 0, s>>>(p);
+    if (inplace) launch(ew_vec_kernel<T, HAS_Y, UNROLL, false, true>, grid, EW_BLOCK, 0, s, p);
+    else launch(ew_vec_kernel<T, HAS_Y, UNROLL, true, true>, grid, EW_BLOCK, 0, s, p);
   } else {
-    if (inplace) ew_vec_kernel<T, HAS_Y, UNROLL, false, false><<<grid, EW_BLOCK, 0, s>>>(p);
-    else ew_vec_kernel<T, HAS_Y, UNROLL, true, false><<<grid, EW_BLOCK, 0, s>>>(p);
+    if (inplace) launch(ew_vec_kernel<T, HAS_Y, UNROLL, false, false>, grid, EW_BLOCK, 0, s, p);
+    else launch(ew_vec_kernel<T, HAS_Y, UNROLL, true, false>, grid, EW_BLOCK, 0, s, p);
   }
   count_launch();
   return check_launch("ew_vec_kernel");

@@ -62,6 +62,7 @@ struct EmArgs {
 
 template <int OP, typename T, int UNROLL, bool NC>
 __global__ void __launch_bounds__(EM_BLOCK) ewmap_vec_kernel(EmArgs<T> p) {
+  pdl_enter();
   constexpr int VEC = 32 / sizeof(T);
   constexpr bool HAS_Y = binary_op<OP>();
   const int64_t tid = (int64_t)blockIdx.x * EM_BLOCK + threadIdx.x;
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(EM_BLOCK) ewmap_vec_kernel(EmArgs<T> p) {
 
 template <int OP, typename T>
 __global__ void __launch_bounds__(EM_BLOCK) ewmap_scalar_kernel(EmArgs<T> p) {
+  pdl_enter();
   constexpr bool HAS_Y = binary_op<OP>();
   const int64_t stride = (int64_t)gridDim.x * EM_BLOCK;
   for (int64_t i = (int64_t)blockIdx.x * EM_BLOCK + threadIdx.x; i < p.n; i += stride)
@@ -120,15 +122,15 @@ ga_status_t run(int64_t n, const void *x, const void *y, void *z, cudaStream_t s
   if (!coaligned) {
     p.head = p.nvec = 0;
     const int grid = (int)std::min<int64_t>(std::max<int64_t>(cdiv(n, EM_BLOCK), 1), (int64_t)sm_count() * 8);
-    ewmap_scalar_kernel<OP, T><<<grid, EM_BLOCK, 0, s>>>(p);
+    launch(ewmap_scalar_kernel<OP, T>, grid, EM_BLOCK, 0, s, p);
   } else {
     p.head = std::min<int64_t>(n, (int64_t)(((32 - phase) & 31) / sizeof(T)));
     p.nvec = (n - p.head) / VEC;
     const int grid = (int)std::min<int64_t>(std::max<int64_t>(cdiv(p.nvec, (int64_t)EM_BLOCK * UNROLL), 1),
                                             0x7fffffffLL);
     const bool inplace = z == x || (HAS_Y && z == y);
-    if (inplace) ewmap_vec_kernel<OP, T, UNROLL, false><<<grid, EM_BLOCK, 0, s>>>(p);
-    else ewmap_vec_kernel<OP, T, UNROLL, true><<<grid, EM_BLOCK, 0, s>>>(p);
+    if (inplace) launch(ewmap_vec_kernel<OP, T, UNROLL, false>, grid, EM_BLOCK, 0, s, p);
+    else launch(ewmap_vec_kernel<OP, T, UNROLL, true>, grid, EM_BLOCK, 0, s, p);
   }
   count_launch();
   return check_launch("ewmap_kernel");

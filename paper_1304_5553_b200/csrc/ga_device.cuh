@@ -12,6 +12,22 @@
 namespace ga {
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch.  Every product kernel is launched with
+// programmatic stream serialization (ga_host.h launch()), so its CTAs may be
+// scheduled while the previous grid of the stream is still finishing.  The
+// first statement of every kernel is pdl_enter(): wait until the previous
+// grid has completed and its memory operations are visible (nothing of this
+// kernel touches global memory before that), then allow the next grid to
+// begin launching — it fires once every CTA of this grid has started, i.e.
+// during the last wave, so the next kernel's launch, CTA dispatch and
+// prologue overlap this kernel's tail instead of following it.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
 // 256-bit memory operations (sm_100: LDG.E.NA.ENL2.256 / STG.E.NA.ENL2.256).
 // Streaming data is touched once, so loads skip L1 allocation.
 // ---------------------------------------------------------------------------

@@ -23,6 +23,25 @@ int resident_grid(const void *kernel, int block, size_t dyn_smem = 0);
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Launch `kernel` on stream s with programmatic stream serialization (PDL):
+// the kernel may begin launching before the previous grid in the stream has
+// finished; its pdl_enter() (ga_device.cuh) waits for that grid before any
+// memory access.  The error, if any, is left for check_launch().
+template <typename... Params, typename... Args>
+inline void launch(void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<Params>(args)...);
+}
+
 inline size_t dtype_size(ga_dtype_t dt) {
   return (dt == GA_F32 || dt == GA_I32) ? 4 : dt == GA_C128 ? 16 : 8;
 }

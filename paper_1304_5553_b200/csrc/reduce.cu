@@ -22,8 +22,9 @@
 //      block of the grid folds the group partials in order, writes *out and
 //      advances the epoch (no second launch, no host sync, no memset
 //      between calls).
-// Deterministic for a given n (the grid depends on n only, not on the
-// device): every fold order above is fixed.
+// Deterministic for a given (n, device): the grid depends on n, the finish's
+// group size also on the device's SM count (make_finish), and every fold
+// order above is fixed by those two.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -48,7 +49,7 @@ constexpr int RED_BLOCK = 256, RED_MINB = 4;
 template <typename Tin, typename Tacc, int OP, int MAP>
 ga_status_t run(int64_t n, const void *x, const void *y, void *out, void *ws, const Exchange &xg, cudaStream_t s) {
   if (n == 0 && xg.world == 0) {
-    neutral_kernel<Tacc, OP><<<1, 1, 0, s>>>(static_cast<Tacc *>(out));
+    launch(neutral_kernel<Tacc, OP>, 1, 1, 0, s, static_cast<Tacc *>(out));
     count_launch();
     return check_launch("neutral_kernel");
   }
@@ -86,7 +87,7 @@ ga_status_t run(int64_t n, const void *x, const void *y, void *out, void *ws, co
   const int64_t units = coaligned ? cdiv(std::max<int64_t>(p.nvec, 1), (int64_t)RED_BLOCK * UNROLL) : cdiv(n, RED_BLOCK);
   const int grid = (int)std::max<int64_t>(std::min<int64_t>(units, RED_MAX_PARTIALS), 1);
   p.fin = make_finish(ws, grid, RED_MINB);
-  kern<<<grid, RED_BLOCK, 0, s>>>(p);
+  launch(kern, grid, RED_BLOCK, 0, s, p);
   count_launch();
   return check_launch("reduce_kernel");
 }

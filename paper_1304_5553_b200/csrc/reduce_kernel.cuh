@@ -300,6 +300,7 @@ __device__ __forceinline__ void grid_finish(Tacc v, uint32_t tag, Tacc *smem, co
 
 template <typename Tin, typename Tacc, int OP, int MAP, int UNROLL, int RED_BLOCK, int MINB>
 __global__ void __launch_bounds__(RED_BLOCK, MINB) reduce_kernel(RedArgs<Tin, Tacc> p) {
+  pdl_enter();
   constexpr int VEC = 32 / sizeof(Tin);
   constexpr bool HAS_Y = MAP == GA_MAP_MUL || MAP == GA_MAP_CONJ_MUL;
   __shared__ Tacc smem[RED_BLOCK / 32];
@@ -379,6 +380,7 @@ __global__ void __launch_bounds__(RED_BLOCK, MINB) reduce_kernel(RedArgs<Tin, Ta
 
 template <typename Tacc, int OP>
 __global__ void neutral_kernel(Tacc *out) {
+  pdl_enter();
   *out = Op<OP, Tacc>::neutral();
 }
 

@@ -79,7 +79,7 @@ ga_status_t run(int64_t n, const void *in, void *out, const void *carry, int64_t
   if (p.num_tiles > 0x7fffffffLL) return fail(GA_ERR_UNSUPPORTED, "scan: n too large (%lld)", (long long)n);
   const int grid = (int)p.num_tiles;
   if constexpr (SHAPE == SHAPE_RG) {
-    scan_reg_kernel<OP, T, Tin, RG_BLOCK, RG_ITEMS, RG_DEPTH, EXCLUSIVE><<<grid, RG_BLOCK, 0, s>>>(p);
+    launch(scan_reg_kernel<OP, T, Tin, RG_BLOCK, RG_ITEMS, RG_DEPTH, EXCLUSIVE>, grid, RG_BLOCK, 0, s, p);
   } else {
     constexpr int W = ShapeOf<SHAPE, T>::WARPS, R = ShapeOf<SHAPE, T>::ROWS;
     constexpr int D = sizeof(T) == 8 ? DEPTH8 : DEPTH4;
@@ -92,9 +92,9 @@ ga_status_t run(int64_t n, const void *in, void *out, const void *carry, int64_t
     constexpr int PF = (SHAPE == SHAPE_L && sizeof(T) == sizeof(Tin)) ? R : 0;
     if (PF) p.pf_dist = std::max<int64_t>(1, (int64_t)sm_count() * 2 / 7);
     if (in == out)
-      scan_l2_kernel<OP, T, Tin, W, R, U, D, false, EXCLUSIVE, true, P1U, PF><<<grid, W * 32, 0, s>>>(p);
+      launch(scan_l2_kernel<OP, T, Tin, W, R, U, D, false, EXCLUSIVE, true, P1U, PF>, grid, W * 32, 0, s, p);
     else
-      scan_l2_kernel<OP, T, Tin, W, R, U, D, true, EXCLUSIVE, true, P1U, PF><<<grid, W * 32, 0, s>>>(p);
+      launch(scan_l2_kernel<OP, T, Tin, W, R, U, D, true, EXCLUSIVE, true, P1U, PF>, grid, W * 32, 0, s, p);
   }
   count_launch();
   return check_launch("scan_kernel");

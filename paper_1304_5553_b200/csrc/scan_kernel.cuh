@@ -346,6 +346,7 @@ __device__ __forceinline__ void draw_tile(const A &p, uint32_t &tile, uint32_t &
 template <int OP, typename T, typename Tin, int WARPS, int ROWS, int UNROLL, int DEPTH, bool NC, bool EXCLUSIVE,
           bool EARLY, int P1U = UNROLL, int PF_ROWS = 0>
 __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p) {
+  pdl_enter();
   using O = Op<OP, T>;
   constexpr int E = Chunk<Tin>::E;  // elements per lane per row
   constexpr int ROW = 32 * E;       // elements per row: 512 bytes of input
@@ -518,6 +519,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p)
 // ===========================================================================
 template <int OP, typename T, typename Tin, int BLOCK, int ITEMS, int DEPTH, bool EXCLUSIVE>
 __global__ void __launch_bounds__(BLOCK, 2) scan_reg_kernel(ScanArgs<T, Tin> p) {
+  pdl_enter();
   using O = Op<OP, T>;
   constexpr int WARPS = BLOCK / 32;
   constexpr int64_t TILE = (int64_t)BLOCK * ITEMS;

@@ -41,6 +41,7 @@ __device__ __forceinline__ T point(const StArgs<T> &p, int64_t i, T xm, T x0, T 
 
 template <typename T>
 __global__ void __launch_bounds__(ST_BLOCK) stencil_vec_kernel(StArgs<T> p) {
+  pdl_enter();
   constexpr int VEC = 32 / sizeof(T);
   const int lane = threadIdx.x & 31;
   const int64_t v = (int64_t)blockIdx.x * ST_BLOCK + threadIdx.x;
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(ST_BLOCK) stencil_vec_kernel(StArgs<T> p) {
 
 template <typename T>
 __global__ void __launch_bounds__(ST_BLOCK) stencil_scalar_kernel(StArgs<T> p) {
+  pdl_enter();
   const int64_t stride = (int64_t)gridDim.x * ST_BLOCK;
   for (int64_t i = (int64_t)blockIdx.x * ST_BLOCK + threadIdx.x; i < p.n; i += stride)
     p.y[i] = point(p, i, i > 0 ? p.x[i - 1] : T(0), p.x[i], i + 1 < p.n ? p.x[i + 1] : T(0));
@@ -103,11 +105,11 @@ ga_status_t run(int64_t n, const ga_scalar_t &l, const ga_scalar_t &d, const ga_
     p.nvec = n / VEC;
     const int64_t threads = std::max<int64_t>(p.nvec, n - p.nvec * VEC);
     const int grid = (int)std::max<int64_t>(cdiv(threads, ST_BLOCK), 1);
-    stencil_vec_kernel<T><<<grid, ST_BLOCK, 0, s>>>(p);
+    launch(stencil_vec_kernel<T>, grid, ST_BLOCK, 0, s, p);
   } else {
     p.nvec = 0;
     const int grid = (int)std::min<int64_t>(std::max<int64_t>(cdiv(n, ST_BLOCK), 1), (int64_t)sm_count() * 16);
-    stencil_scalar_kernel<T><<<grid, ST_BLOCK, 0, s>>>(p);
+    launch(stencil_scalar_kernel<T>, grid, ST_BLOCK, 0, s, p);
   }
   count_launch();
   return check_launch("stencil_kernel");

@@ -58,3 +58,65 @@ def chunk_sums_int(n, kind, seed, lo, hi, chunk, procs=None):
     with mp.get_context("spawn").Pool(procs) as pool:
         parts = pool.map(_job, jobs, chunksize=1)
     return [int(p[0]) for p in parts]
+
+
+def _scan_cmp_job(args):
+    """Compare one chunk of a GPU scan output (already in shared memory)
+    element by element with the oracle's scan of the regenerated chunk."""
+    from multiprocessing import shared_memory
+    import oracle
+    import synth
+    (shm_name, off, kind, seed, lo, hi, start, m, carry, exclusive, out_dtype) = args
+    odt = np.dtype(out_dtype)
+    shm = shared_memory.SharedMemory(name=shm_name)
+    try:
+        got = np.ndarray((m,), dtype=odt, buffer=shm.buf, offset=off)
+        x = synth.host_fill(kind, seed, m, start=start, lo=lo, hi=hi)
+        ref = oracle.scan(oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE, x, carry=odt.type(carry),
+                          out_dtype=odt if odt != x.dtype else None)
+        bad = np.flatnonzero(got != ref)
+        res = (start, int(bad.size), int(start + bad[0]) if bad.size else -1)
+        del got
+        return res
+    finally:
+        shm.close()
+
+
+def chunked_scan_compare(fetch, n, kind, seed, lo, hi, out_dtype, exclusive, chunk=CHUNK, batch=32, procs=None):
+    """Element-by-element comparison of a whole integer scan output of n
+    elements against the chunked oracle: every chunk's carry-in is the exact
+    (wrapped) sum of the chunks before it, and the oracle scans each
+    regenerated chunk from that carry.  `fetch(start, m, dest)` copies output
+    elements [start, start+m) into the numpy array `dest`.  The output
+    streams through a shared-memory window of `batch` chunks.  Returns
+    (elements compared, mismatches, first mismatching index or -1)."""
+    from multiprocessing import shared_memory
+    odt = np.dtype(out_dtype)
+    w = 1 << (odt.itemsize * 8)
+    sums = chunk_sums_int(n, kind, seed, lo, hi, chunk, procs=procs)
+    carries, prefix = [], 0
+    for s in sums:
+        carries.append(((prefix + w // 2) % w) - w // 2)
+        prefix += s
+    starts = list(range(0, n, chunk))
+    procs = procs or max(1, min(len(os.sched_getaffinity(0)), 32))
+    shm = shared_memory.SharedMemory(create=True, size=batch * chunk * odt.itemsize)
+    compared, mismatches, first = 0, 0, -1
+    try:
+        with mp.get_context("spawn").Pool(procs) as pool:
+            for b0 in range(0, len(starts), batch):
+                jobs = []
+                for j, start in enumerate(starts[b0:b0 + batch]):
+                    m = min(chunk, n - start)
+                    off = j * chunk * odt.itemsize
+                    fetch(start, m, np.ndarray((m,), dtype=odt, buffer=shm.buf, offset=off))
+                    jobs.append((shm.name, off, kind, seed, lo, hi, start, m, carries[b0 + j], exclusive, odt.str))
+                for start, bad, idx in pool.map(_scan_cmp_job, jobs, chunksize=1):
+                    compared += min(chunk, n - start)
+                    mismatches += bad
+                    if bad and (first < 0 or idx < first):
+                        first = idx
+    finally:
+        shm.close()
+        shm.unlink()
+    return compared, mismatches, first

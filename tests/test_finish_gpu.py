@@ -83,3 +83,52 @@ def test_float_sum_deterministic_across_group_shapes():
     x = synth.device_fill(synth.F32_S11, 3, n, device=DEV)
     vals = {float(G.reduce(G.SUM, G.ID, x).item()) for _ in range(8)}
     assert len(vals) == 1
+
+
+def test_concurrent_large_reductions_on_four_streams():
+    """Four multi-group reductions at 2^30 elements run concurrently on four
+    streams (256 groups each, 4 x 256 group leaders against ~592 resident
+    blocks), ten rounds without a host sync: the finish must make progress
+    and every result must be exact (int) / within R10 (float).  Progress
+    rests on blocks being dispatched in index order within a grid (a group
+    leader is its group's last block, so every block it waits for is already
+    resident, whatever the other grids hold; R29)."""
+    n = 1 << 30
+    free, _ = torch.cuda.mem_get_info()
+    if free < 4 * n * 4 * 1.1:
+        pytest.skip("needs 16 GiB of free device memory")
+    xi = synth.device_fill(synth.I32_RANGE, 31, n, lo=-(1 << 15), hi=(1 << 15) - 1, device=DEV)
+    xj = synth.device_fill(synth.I32_RANGE, 32, n, lo=-(1 << 15), hi=(1 << 15) - 1, device=DEV)
+    xf = synth.device_fill(synth.F32_U01, 33, n, device=DEV)
+    yf = synth.device_fill(synth.F32_U01, 34, n, device=DEV)
+    rounds = 10
+    outs = [torch.empty(rounds, dtype=dt, device=DEV)
+            for dt in (torch.int32, torch.int32, torch.float32, torch.float32)]
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    torch.cuda.synchronize()
+    for r in range(rounds):
+        calls = [lambda o: G.reduce(G.SUM, G.ID, xi, out=o), lambda o: G.reduce(G.MAX, G.ID, xj, out=o),
+                 lambda o: G.reduce(G.SUM, G.MUL, xf, yf, out=o), lambda o: G.reduce(G.SUM, G.SQUARE, xf, out=o)]
+        for s, call, o in zip(streams, calls, outs):
+            with torch.cuda.stream(s):
+                call(o[r:r + 1])
+    torch.cuda.synchronize()
+    got = [o.cpu().numpy() for o in outs]
+    del xi, xj, xf, yf
+    torch.cuda.empty_cache()
+    import bigcheck
+    ref_i, _ = bigcheck.chunked_reduce(oracle.SUM, oracle.MAP_ID, n, synth.I32_RANGE, 31, lo=-(1 << 15),
+                                       hi=(1 << 15) - 1, out_dtype=np.int32)
+    ref_j, _ = bigcheck.chunked_reduce(oracle.MAX, oracle.MAP_ID, n, synth.I32_RANGE, 32, lo=-(1 << 15),
+                                       hi=(1 << 15) - 1)
+    ref_d, _ = bigcheck.chunked_reduce(oracle.SUM, oracle.MAP_MUL, n, synth.F32_U01, 33, kind_y=synth.F32_U01,
+                                       seed_y=34)
+    ref_n, _ = bigcheck.chunked_reduce(oracle.SUM, oracle.MAP_SQUARE, n, synth.F32_U01, 33)
+    assert all(int(v) == ref_i for v in got[0])
+    assert all(int(v) == ref_j for v in got[1])
+    for v in got[2]:
+        assert abs(float(v) - ref_d) <= 1e-5 * abs(ref_d)
+    for v in got[3]:
+        assert abs(float(v) - ref_n) <= 1e-5 * abs(ref_n)
+    # a fixed fold order per (grid, group): every round gives the same bits
+    assert len(set(got[2].tolist())) == 1 and len(set(got[3].tolist())) == 1

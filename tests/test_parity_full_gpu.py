@@ -3,12 +3,13 @@ same launch configurations) bench.py times.  The oracle cannot hold or scan
 2^33 elements in one go, so it runs chunk-wise over regenerated inputs
 (tests/bigcheck.py); outputs too large to compare whole are checked on
 sampled windows whose exact expected values the chunked oracle provides,
-plus properties that hold at any size.
+plus properties that hold at any size; integer scans are compared whole,
+element by element, against the chunked oracle (bigcheck.chunked_scan_compare).
 
   C2  fp32/fp64 axpbyz (full, bit-exact) and norm2 (tolerance) on n = 2^28
   C3  int32/int64 sum (exact), max (exact, planted), inclusive scan on n = 2^30
   C4  fp32 dot + norm2 on n = 2^33 (one GPU holds both 32 GiB inputs)
-  C5  int32 exclusive scan on n = 2^33 (windows at every 2^25 boundary)
+  C5  int32 exclusive scan on n = 2^33 (every element, chunked oracle)
   bench step: axpbyz(5, x, 6, y) + dot + sum + norm2 + exclusive scan at 2^28."""
 import math
 
@@ -117,7 +118,16 @@ def test_c3_int_sum_max_scan_2p30(dt):
     out = G.scan(k)
     del k
     free()
-    _check_scan_windows(out, n, kind, 3, 0, 9, npdt, exclusive=False)
+    _check_scan_full(out, n, kind, 3, 0, 9, npdt, exclusive=False)
+
+
+def _check_scan_full(out, n, kind, seed, lo, hi, npdt, exclusive):
+    """Every element of the device scan output against the chunked oracle."""
+    def fetch(start, m, dest):
+        torch.from_numpy(dest).copy_(out[start:start + m])
+    compared, bad, first = bigcheck.chunked_scan_compare(fetch, n, kind, seed, lo, hi, npdt, exclusive)
+    assert compared == n
+    assert bad == 0, f"{bad} of {n} elements differ, first at {first}"
 
 
 def _check_scan_windows(out, n, kind, seed, lo, hi, npdt, exclusive, window=1 << 16, widen=False):
@@ -157,7 +167,7 @@ def test_c3_widening_scan_2p30():
     del k
     free()
     assert int(out[-1].item()) > (1 << 31)
-    _check_scan_windows(out, n, synth.I32_RANGE, 3, 0, 9, np.int64, exclusive=False, widen=True)
+    _check_scan_full(out, n, synth.I32_RANGE, 3, 0, 9, np.int64, exclusive=False)
 
 
 def test_c4_dot_norm2_2p33():
@@ -183,7 +193,7 @@ def test_c5_exclusive_scan_2p33():
     out = G.scan(k, exclusive=True)
     del k
     free()
-    _check_scan_windows(out, n, synth.I32_RANGE, 3, 0, 9, np.int32, exclusive=True, window=1 << 14)
+    _check_scan_full(out, n, synth.I32_RANGE, 3, 0, 9, np.int32, exclusive=True)
     del out
     free()
 
