@@ -92,9 +92,11 @@ ga_status_t run(int64_t n, const void *in, void *out, const void *carry, int64_t
     constexpr int PF = (SHAPE == SHAPE_L && sizeof(T) == sizeof(Tin)) ? R : 0;
     if (PF) p.pf_dist = std::max<int64_t>(1, (int64_t)sm_count() * 2 / 7);
     if (in == out)
-      launch(scan_l2_kernel<OP, T, Tin, W, R, U, D, false, EXCLUSIVE, true, P1U, PF>, grid, W * 32, 0, s, p);
+      launch(scan_l2_kernel<OP, T, Tin, W, R, U, D, false, EXCLUSIVE, true, P1U, PF>, grid, W * 32, 0, s, p,
+             (uint64_t *)nullptr);
     else
-      launch(scan_l2_kernel<OP, T, Tin, W, R, U, D, true, EXCLUSIVE, true, P1U, PF>, grid, W * 32, 0, s, p);
+      launch(scan_l2_kernel<OP, T, Tin, W, R, U, D, true, EXCLUSIVE, true, P1U, PF>, grid, W * 32, 0, s, p,
+             (uint64_t *)nullptr);
   }
   count_launch();
   return check_launch("scan_kernel");

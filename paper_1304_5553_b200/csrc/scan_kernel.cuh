@@ -344,8 +344,8 @@ __device__ __forceinline__ void draw_tile(const A &p, uint32_t &tile, uint32_t &
 // P1U: rows in flight per warp in phase 1 (its only live state is the raw
 // rows, so it can exceed phase 3's UNROLL).
 template <int OP, typename T, typename Tin, int WARPS, int ROWS, int UNROLL, int DEPTH, bool NC, bool EXCLUSIVE,
-          bool EARLY, int P1U = UNROLL, int PF_ROWS = 0>
-__global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p) {
+          bool EARLY, int P1U = UNROLL, int PF_ROWS = 0, bool TRACE = false>
+__global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p, uint64_t *trace) {
   pdl_enter();
   using O = Op<OP, T>;
   constexpr int E = Chunk<Tin>::E;  // elements per lane per row
@@ -369,6 +369,21 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p)
   __syncthreads();
   const int64_t tile = s_tile;
   const uint32_t epoch = s_epoch;
+  // TRACE (tools/lab/trace_l2.py only; compiled out otherwise): per tile
+  // {start, phase 1 done, prefix known, stored, -, -, -, SM id} in ns
+  auto stamp = [&](int k) {
+    if constexpr (TRACE) {
+      if (threadIdx.x == 0) trace[tile * 8 + k] = globaltimer_ns();
+    }
+  };
+  if constexpr (TRACE) {
+    if (threadIdx.x == 0) {
+      uint32_t sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      trace[tile * 8 + 7] = sm;
+    }
+  }
+  stamp(0);
   const int64_t slice0 = tile * TILE + (int64_t)warp * ROWS * ROW;  // first element of my slice
   const bool full = tile * TILE + TILE <= p.n;
   const uint64_t keep = l2::policy_evict_last();
@@ -410,6 +425,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p)
   acc = warp_fold<OP, T>(acc);
   if (lane == 0) s_slice[warp] = acc;
   __syncthreads();
+  stamp(1);
 
   // While warp 0 looks back (the SM has no HBM reads in flight then), every
   // warp asks the TMA unit to pull the first PF_ROWS rows of its slice of the
@@ -444,6 +460,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p)
       if (lane == 0) p.status.publish(tile, epoch, FLAG_INCLUSIVE, O::fold(prefix, total));
     }
     if (lane < WARPS) s_slice[lane] = O::fold(prefix, wex);  // exclusive prefix of slice `lane`
+    stamp(2);
   }
 
   // phase 3 helpers.  load_local: rows [r0, r0+UNROLL) into registers (raw),
@@ -511,6 +528,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p)
     store_chunk(r0, v, off, base);
     base = O::fold(base, ctot);
   }
+  stamp(3);
 }
 
 // ===========================================================================

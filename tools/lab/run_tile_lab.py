@@ -10,7 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
-LIB = os.path.join(HERE, "libtile_lab.so")
+LIB = os.environ.get("TILE_LAB_LIB", os.path.join(HERE, "libtile_lab.so"))
 
 
 def build():

@@ -13,7 +13,7 @@ static int run(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   constexpr int64_t TILE = (int64_t)W * R * 512 / sizeof(T);
   ScanArgs<T> p = make_args<T>(n, TILE, in, out, nullptr, 0, ws);
   p.pf_dist = PF_DIST;
-  scan_l2_kernel<GA_OP_SUM, T, T, W, R, U, D, true, true, true, P1U, PF><<<(int)p.num_tiles, W * 32, 0, s>>>(p);
+  scan_l2_kernel<GA_OP_SUM, T, T, W, R, U, D, true, true, true, P1U, PF><<<(int)p.num_tiles, W * 32, 0, s>>>(p, nullptr);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : 100 + (int)e;
 }
@@ -84,3 +84,20 @@ extern "C" int64_t lab_scan_tile(int v) {
   return 0;
 }
 extern "C" int lab_scan_elem_bytes(int v) { return ((v >= 20 && v < 30) || v == 46 || v >= 50) ? 8 : 4; }
+
+// the product configuration (L shape, int32, exclusive, 32 rows prefetched 42
+// ids ahead; v == 1: no prefetch) compiled with TRACE: per tile {start,
+// phase 1 done, prefix known, stored, -, -, -, SM id} (tools/lab/trace_l2.py)
+extern "C" int lab_scan_trace(int v, int64_t n, const void *in, void *out, void *ws, void *trace, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  constexpr int64_t TILE = 24 * 32 * 512 / 4;
+  ScanArgs<int32_t> p = make_args<int32_t>(n, TILE, in, out, nullptr, 0, ws);
+  p.pf_dist = v == 1 ? 0 : 42;
+  if (v == 1)
+    scan_l2_kernel<GA_OP_SUM, int32_t, int32_t, 24, 32, 8, 8, true, true, true, 8, 0, true>
+        <<<(int)p.num_tiles, 24 * 32, 0, s>>>(p, (uint64_t *)trace);
+  else
+    scan_l2_kernel<GA_OP_SUM, int32_t, int32_t, 24, 32, 8, 8, true, true, true, 8, 32, true>
+        <<<(int)p.num_tiles, 24 * 32, 0, s>>>(p, (uint64_t *)trace);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
