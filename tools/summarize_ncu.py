@@ -1,6 +1,11 @@
 """Summarise ncu captures into profiles/ (committed evidence).
 
     python tools/summarize_ncu.py <round-tag> <full.ncu-rep> [launches.csv]
+    python tools/summarize_ncu.py traffic <log2n> <metrics.csv>
+
+The second form reads an `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum
+--csv` log of the bench's five hot-path launches at another size and records
+their DRAM bytes per launch in profiles/ncu_traffic.json under <op>@2^<log2n>.
 
 Writes profiles/<tag>_kernels.md (per-kernel metrics of the --set full
 capture), profiles/<tag>_launches.md (share of each kernel in the launch
@@ -55,13 +60,41 @@ def to_bytes(v, unit):
     return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
 
 
+def traffic_from_metrics(log2n, path):
+    text = open(path).read()
+    start = text.find('"ID"')
+    rows = list(csv.reader(io.StringIO(text[start:])))
+    h = rows[0]
+    ki, ni, vi, ui = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
+    ii = h.index("ID")
+    per = defaultdict(dict)
+    names = {}
+    for r in rows[1:]:
+        if len(r) <= vi:
+            continue
+        per[r[ii]][r[ni]] = to_bytes(r[vi].replace(",", ""), r[ui]) if "bytes" in r[ni] else r[vi]
+        names[r[ii]] = r[ki]
+    traffic_path = os.path.join(PROF, "ncu_traffic.json")
+    traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    seen = set()
+    for i in sorted(per, key=int):
+        op = op_of(names[i])
+        if op in OPS and op not in seen:
+            seen.add(op)
+            traffic[f"{op}@2^{log2n}"] = int(per[i]["dram__bytes_read.sum"] + per[i]["dram__bytes_write.sum"])
+            print(op, log2n, traffic[f"{op}@2^{log2n}"])
+    json.dump(traffic, open(traffic_path, "w"), indent=1, sort_keys=True)
+
+
 def main():
+    if sys.argv[1] == "traffic":
+        return traffic_from_metrics(int(sys.argv[2]), sys.argv[3])
     tag, rep = sys.argv[1], sys.argv[2]
     launches = sys.argv[3] if len(sys.argv) > 3 else None
     os.makedirs(PROF, exist_ok=True)
     hdr, units, rows = raw_rows(rep)
     idx = {k: hdr.index(k) for k, _ in KEYS if k in hdr}
-    lines = [f"# {tag}: ncu --set full --clock-control none (one launch per kernel, n = 2^28)", "",
+    lines = [f"# {tag}: ncu --set full --clock-control none (one launch per kernel, n = 2^28, `tools/profile_ops.py 28`)", "",
              "Source: `" + os.path.basename(rep) + "` (gpurun_out/, not committed). Durations are ncu's "
              "(serialised, cold-ish L2); compare shares, not absolutes, with bench.py.", "",
              "| op | kernel | " + " | ".join(n for _, n in KEYS) + " | DRAM GB/s |", "|" + "---|" * (len(KEYS) + 3)]
@@ -106,7 +139,7 @@ def main():
                "`ncu --metrics gpu__time_duration.sum --clock-control none`", "",
                "Cold-cache, serialised per-launch times: the SHARE column of the step table is what must agree "
                "with bench.py's per-op split (ops.*.ms).", ""]
-        for name, title in (("step", "Bench step (first 6 launches of each op: 3 warm-up + 3 timed steps, n = 2^28)"),
+        for name, title in (("step", "Bench step (first 6 launches of each op: 3 warm-up + 3 timed steps, n = 2^33 per GPU)"),
                             ("all", "Every launch of the command (incl. the input fills and the e2e pipeline's "
                                     "2^24-element chunks)")):
             tot, cnt = tables[name]
