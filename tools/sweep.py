@@ -4,6 +4,11 @@ on the launching stream; when the working set is smaller than 4x L2 the L2 is
 flushed before every timed call — a 512 MiB write, then a 512 MiB read of
 another buffer so that the dirty lines of the write are written back before
 the timed region (otherwise the op pays for them) — and only the op is timed.
+Before every timed call the GPU is also given ~10 us of work (a device-side
+sleep) so that the host enqueues the start event, the op and the stop event
+while the stream is busy: the event interval then holds the op's device time,
+not the host's launch latency (round 1's unflushed points, n >= 2^26 here,
+included ~5 us of it).
 
     python tools/sweep.py [--min 16] [--max 30] [--reps 20] [--out gpurun_out/sweep.json]
 """
@@ -84,6 +89,7 @@ def main():
                 if small:
                     flush.fill_(1.0)
                     G.sum(clean, out=sink)
+                torch.cuda._sleep(20000)  # ~10 us of device time ahead of e0
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 fn()

@@ -9,7 +9,8 @@ lgs = sorted({r["log2n"] for r in rows})
 d = {(r["op"], r["dtype"], r["log2n"]): r for r in rows}
 out = ["# HBM-roofline sweep, n = 2^16 .. 2^30 (one B200)", "",
        "`python tools/sweep.py`: median of 15 CUDA-event-timed calls per point; working sets below 4x L2 are "
-       "flushed (512 MiB write, then a 512 MiB read of another buffer) before every call.  Algorithmic GB/s "
+       "flushed (512 MiB write, then a 512 MiB read of another buffer) before every call, and a ~10 us device sleep "
+       "precedes every timed call so the events measure device time, not host launch latency.  Algorithmic GB/s "
        "(axpbyz 12/24 B, dot 8, sum/norm2 4/8, scan 8/16 B per element).  Small n is launch- and "
        "latency-bound (a 2^16 fp32 sum is 256 KiB).", "",
        "| op | dtype | " + " | ".join(f"2^{l}" for l in lgs) + " |", "|---|---|" + "---|" * len(lgs)]
