@@ -26,8 +26,8 @@
  * something other than itself — numpy's uncontracted arithmetic, math.fsum,
  * fractions.Fraction brute force, Python big-int arithmetic, closed forms
  * (ramp sums, constant-times-ramp dot, all-ones scan) and SPEC.md worked
- * values.  Exception: the sign of a zero max/min result — "parity unpinned"
- * (R7; either zero accepted).
+ * values; MAX/MIN, including the sign of a zero result (R7), against a
+ * Python brute force that orders values by (value, sign) with NaN dropped.
  */
 #include <math.h>
 #include <stdint.h>
@@ -37,6 +37,35 @@ enum { O_F32 = 0, O_F64 = 1, O_I32 = 2, O_I64 = 3 };
 enum { O_SUM = 0, O_MAX = 1, O_MIN = 2 };
 enum { O_MAP_ID = 0, O_MAP_MUL = 1, O_MAP_SQUARE = 2 };
 enum { O_INCLUSIVE = 0, O_EXCLUSIVE = 1 };
+
+/* maximumNumber / minimumNumber (IEEE 754-2019 §9.6; R6, R7): the
+ * larger / smaller operand; a NaN operand loses to a number; -0 is less than
+ * +0.  A total order on the non-NaN values, so a fold's result does not
+ * depend on the fold order (the GPU folds in tree order). */
+static float max_num_f32(float a, float b) {
+  if (isnan(a)) return b;
+  if (isnan(b)) return a;
+  if (a == b) return signbit(a) ? b : a; /* +0 beats -0; equal values are equal */
+  return a > b ? a : b;
+}
+static float min_num_f32(float a, float b) {
+  if (isnan(a)) return b;
+  if (isnan(b)) return a;
+  if (a == b) return signbit(a) ? a : b; /* -0 beats +0 */
+  return a < b ? a : b;
+}
+static double max_num_f64(double a, double b) {
+  if (isnan(a)) return b;
+  if (isnan(b)) return a;
+  if (a == b) return signbit(a) ? b : a;
+  return a > b ? a : b;
+}
+static double min_num_f64(double a, double b) {
+  if (isnan(a)) return b;
+  if (isnan(b)) return a;
+  if (a == b) return signbit(a) ? a : b;
+  return a < b ? a : b;
+}
 
 /* ------------------------------------------------------------------------ */
 /* Elementwise, §3.2.4.  Statement per index i:           */
@@ -187,8 +216,8 @@ int64_t oracle_sum_int(int map, int in_dt, int out_dt, int64_t n, const void *x,
 /* ------------------------------------------------------------------------ */
 /* Map-reduce MAX / MIN.  Fold from the neutral element:    */
 /* MAX: -inf / INT_MIN; MIN: +inf / INT_MAX (R5).  The map is evaluated in    */
-/* the input dtype, RN_T(x*y) (R3).  Floats fold with fmax/fmin (maxNum:      */
-/* the non-NaN operand wins, R6).                                             */
+/* the input dtype, RN_T(x*y) (R3).  Floats fold with maximumNumber /        */
+/* minimumNumber (the non-NaN operand wins, R6; -0 < +0, R7).                 */
 /* ------------------------------------------------------------------------ */
 double oracle_maxmin_f32(int op, int map, int64_t n, const float *x, const float *y) {
   float acc = (op == O_MAX) ? -INFINITY : INFINITY;
@@ -197,7 +226,7 @@ double oracle_maxmin_f32(int op, int map, int64_t n, const float *x, const float
     if (map == O_MAP_ID) t = x[i];
     else if (map == O_MAP_MUL) t = x[i] * y[i];
     else t = x[i] * x[i];
-    acc = (op == O_MAX) ? fmaxf(acc, t) : fminf(acc, t);
+    acc = (op == O_MAX) ? max_num_f32(acc, t) : min_num_f32(acc, t);
   }
   return (double)acc;
 }
@@ -209,7 +238,7 @@ double oracle_maxmin_f64(int op, int map, int64_t n, const double *x, const doub
     if (map == O_MAP_ID) t = x[i];
     else if (map == O_MAP_MUL) t = x[i] * y[i];
     else t = x[i] * x[i];
-    acc = (op == O_MAX) ? fmax(acc, t) : fmin(acc, t);
+    acc = (op == O_MAX) ? max_num_f64(acc, t) : min_num_f64(acc, t);
   }
   return acc;
 }
@@ -272,7 +301,7 @@ void oracle_scan_i64(int kind, int64_t n, const int64_t *in, int64_t *out, int64
 /* NEXT-2; the paper's scan facility takes a "scan expression" like the      */
 /* reduction's, P:496-499 with P:479-485).                                    */
 /*   MAX / MIN, any dtype: running fold from the neutral element (or the     */
-/*     carry-in), maxNum/minNum for floats (R6) — exact.                      */
+/*     carry-in), maximumNumber/minimumNumber for floats (R6, R7) — exact.    */
 /*   SUM over floats: the exact prefix sums S_i = c + x_0 + ... + x_i,        */
 /*     accumulated with Neumaier compensation in float64 and returned as      */
 /*     float64 (the GPU's tree/look-back order is an approximation of them;   */
@@ -283,11 +312,11 @@ void oracle_scan_maxmin_f32(int op, int kind, int64_t n, const float *in, float 
   for (int64_t i = 0; i < n; ++i) {
     float v = in[i];
     if (kind == O_INCLUSIVE) {
-      acc = (op == O_MAX) ? fmaxf(acc, v) : fminf(acc, v);
+      acc = (op == O_MAX) ? max_num_f32(acc, v) : min_num_f32(acc, v);
       out[i] = acc;
     } else {
       out[i] = acc;
-      acc = (op == O_MAX) ? fmaxf(acc, v) : fminf(acc, v);
+      acc = (op == O_MAX) ? max_num_f32(acc, v) : min_num_f32(acc, v);
     }
   }
 }
@@ -297,11 +326,11 @@ void oracle_scan_maxmin_f64(int op, int kind, int64_t n, const double *in, doubl
   for (int64_t i = 0; i < n; ++i) {
     double v = in[i];
     if (kind == O_INCLUSIVE) {
-      acc = (op == O_MAX) ? fmax(acc, v) : fmin(acc, v);
+      acc = (op == O_MAX) ? max_num_f64(acc, v) : min_num_f64(acc, v);
       out[i] = acc;
     } else {
       out[i] = acc;
-      acc = (op == O_MAX) ? fmax(acc, v) : fmin(acc, v);
+      acc = (op == O_MAX) ? max_num_f64(acc, v) : min_num_f64(acc, v);
     }
   }
 }
@@ -499,8 +528,8 @@ void oracle_ewmap_f32(int op, int64_t n, const float *x, const float *y, float *
       case 6: r = logf(a); break;
       case 7: r = sinf(a); break;
       case 8: r = cosf(a); break;
-      case 9: r = fmaxf(a, b); break;
-      case 10: r = fminf(a, b); break;
+      case 9: r = max_num_f32(a, b); break;
+      case 10: r = min_num_f32(a, b); break;
     }
     z[i] = r;
   }
@@ -519,8 +548,8 @@ void oracle_ewmap_f64(int op, int64_t n, const double *x, const double *y, doubl
       case 6: r = log(a); break;
       case 7: r = sin(a); break;
       case 8: r = cos(a); break;
-      case 9: r = fmax(a, b); break;
-      case 10: r = fmin(a, b); break;
+      case 9: r = max_num_f64(a, b); break;
+      case 10: r = min_num_f64(a, b); break;
     }
     z[i] = r;
   }

@@ -276,6 +276,84 @@ def test_float_maxmin_planted_and_nan():
     assert np.fmax(np.float32(-np.inf), np.fmax(np.float32(-np.inf), np.float32(np.nan))) == -np.inf
 
 
+# MAX / MIN with signed zeros (R7): IEEE 754-2019 maximumNumber /
+# minimumNumber — NaN loses, -0 < +0.  Pinned against a brute force that
+# knows nothing of the C code: Python's max/min over the non-NaN values keyed
+# by (value, copysign(1, value)), so +0 ranks above -0.
+def _key(v):
+    return (float(v), math.copysign(1.0, float(v)))
+
+
+def _brute_max(vals, neutral):
+    vals = [v for v in vals if not math.isnan(float(v))]
+    return max(vals, key=_key) if vals else neutral
+
+
+def _brute_min(vals, neutral):
+    vals = [v for v in vals if not math.isnan(float(v))]
+    return min(vals, key=_key) if vals else neutral
+
+
+def _zeros_heavy(dt, n, seed):
+    rng = np.random.default_rng(seed)
+    tiny = np.finfo(dt).tiny
+    pool = np.array([-0.0, 0.0, -0.0, 0.0, -1.0, 1.0, np.nan, -tiny, tiny], dtype=dt)
+    return pool[rng.integers(0, pool.size, size=n)]
+
+
+def _same_bits(a, b, dt):
+    return np.array(a, dt).tobytes() == np.array(b, dt).tobytes()
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_maxmin_signed_zero_pairs(dt):
+    """The four +-0 pairs in both operand orders, elementwise and folded."""
+    p, m = dt(0.0), dt(-0.0)
+    for a, b in ((p, m), (m, p), (p, p), (m, m)):
+        x, y = np.array([a], dt), np.array([b], dt)
+        want_max = p if (not np.signbit(a) or not np.signbit(b)) else m
+        want_min = m if (np.signbit(a) or np.signbit(b)) else p
+        assert _same_bits(oracle.ewmap(oracle.EW_MAX, x, y)[0], want_max, dt)
+        assert _same_bits(oracle.ewmap(oracle.EW_MIN, x, y)[0], want_min, dt)
+        xy = np.array([a, b], dt)
+        assert _same_bits(oracle.reduce(oracle.MAX, oracle.MAP_ID, xy), want_max, dt)
+        assert _same_bits(oracle.reduce(oracle.MIN, oracle.MAP_ID, xy), want_min, dt)
+    # (+0) * (-1) = -0 under the x*y map: the product's sign counts too
+    x, y = np.array([0.0, 0.0], dt), np.array([-1.0, 1.0], dt)
+    assert _same_bits(oracle.reduce(oracle.MAX, oracle.MAP_MUL, x, y), p, dt)
+    assert _same_bits(oracle.reduce(oracle.MIN, oracle.MAP_MUL, x, y), m, dt)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("mp", [oracle.MAP_ID, oracle.MAP_MUL, oracle.MAP_SQUARE])
+def test_maxmin_signed_zero_brute_force(dt, mp):
+    for seed in range(6):
+        x, y = _zeros_heavy(dt, 501, seed), _zeros_heavy(dt, 501, seed + 100)
+        with np.errstate(all="ignore"):
+            t = x if mp == oracle.MAP_ID else (x * y if mp == oracle.MAP_MUL else x * x)
+        assert _same_bits(oracle.reduce(oracle.MAX, mp, x, y), _brute_max(t, dt(-np.inf)), dt)
+        assert _same_bits(oracle.reduce(oracle.MIN, mp, x, y), _brute_min(t, dt(np.inf)), dt)
+        # any order of the same values gives the same bits (a total order)
+        perm = np.random.default_rng(seed).permutation(x.size)
+        assert _same_bits(oracle.reduce(oracle.MAX, mp, x[perm], y[perm]), oracle.reduce(oracle.MAX, mp, x, y), dt)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("op", [oracle.MAX, oracle.MIN])
+def test_scan_and_ewmap_maxmin_signed_zero_brute_force(dt, op):
+    x, y = _zeros_heavy(dt, 700, 7 + op), _zeros_heavy(dt, 700, 8 + op)
+    brute = _brute_max if op == oracle.MAX else _brute_min
+    neutral = dt(-np.inf) if op == oracle.MAX else dt(np.inf)
+    inc = oracle.scan(oracle.INCLUSIVE, x, op=op)
+    exc = oracle.scan(oracle.EXCLUSIVE, x, op=op)
+    for i in range(x.size):
+        assert _same_bits(inc[i], brute(list(x[:i + 1]), neutral), dt), i
+        assert _same_bits(exc[i], brute(list(x[:i]), neutral), dt), i
+    ew = oracle.ewmap(oracle.EW_MAX if op == oracle.MAX else oracle.EW_MIN, x, y)
+    for i in range(x.size):
+        assert _same_bits(ew[i], brute([x[i], y[i]], dt(np.nan)), dt), i
+
+
 def test_float_maxmin_empty_is_neutral():
     assert oracle.reduce(oracle.MAX, oracle.MAP_ID, np.zeros(0, np.float32)) == -np.inf
     assert oracle.reduce(oracle.MIN, oracle.MAP_ID, np.zeros(0)) == np.inf

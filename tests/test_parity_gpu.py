@@ -205,8 +205,8 @@ def test_maxmin_bit_exact(dt, op, mp, n):
         y = rng.integers(info.min, info.max, size=n, dtype=dt, endpoint=True)
     got = G.reduce(op, mp, to_dev(x), to_dev(y, 2) if mp == G.MUL else None).cpu().numpy()
     ref = oracle.reduce(op, mp, x, y)
-    if np.dtype(dt).kind == "f":
-        assert got == ref or (got == 0 and ref == 0)  # sign of a zero extreme: unpinned (R7)
+    if np.dtype(dt).kind == "f":  # bit-exact, the sign of a zero extreme included (R7)
+        assert np.array(got, dt).tobytes() == np.array(ref, dt).tobytes(), (got, ref)
     else:
         assert int(got) == ref
 
@@ -617,3 +617,56 @@ def test_ewmap_special_values_and_inplace():
     G.sqrt(G.fabs(xd, out=xd), out=xd)
     with np.errstate(all="ignore"):
         assert_bit_exact(xd.cpu().numpy(), np.sqrt(np.abs(x[np.isfinite(x)])))
+
+
+# ------------------------------------------------------------ signed zeros and NaN in MAX / MIN (R6, R7)
+def zeros_heavy(dt, n, seed):
+    """Values from {-0, +0, -1, +1, NaN, -tiny, +tiny} with many signed zeros:
+    every max/min tie is a +-0 tie, which only R7's -0 < +0 decides."""
+    rng = np.random.default_rng(seed)
+    tiny = np.finfo(dt).tiny
+    pool = np.array([-0.0, 0.0, -0.0, 0.0, -1.0, 1.0, np.nan, -tiny, tiny], dtype=dt)
+    return pool[rng.integers(0, pool.size, size=n)]
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("op", [oracle.MAX, oracle.MIN])
+@pytest.mark.parametrize("mp", [oracle.MAP_ID, oracle.MAP_MUL])
+@pytest.mark.parametrize("n", [3, 4097, 300_001])
+@pytest.mark.parametrize("only_zeros", [False, True])
+def test_maxmin_signed_zero_bit_exact(dt, op, mp, n, only_zeros):
+    """Bit-exact max/min over data whose extreme is a signed zero (only_zeros:
+    nothing but -0 and +0, so the result is +0 for MAX and -0 for MIN whenever
+    both occur, whatever the tree order)."""
+    x = zeros_heavy(dt, n, n + op)
+    y = zeros_heavy(dt, n, n + 11)
+    if only_zeros:
+        x = np.where(np.arange(n) % 3 == 0, dt(0.0), dt(-0.0)).astype(dt)
+        y = np.where(np.arange(n) % 5 == 0, dt(-1.0), dt(1.0)).astype(dt)
+    got = G.reduce(op, mp, to_dev(x), to_dev(y) if mp == G.MUL else None).cpu().numpy()
+    ref = oracle.reduce(op, mp, x, y)
+    assert np.array(got, dt).tobytes() == np.array(ref, dt).tobytes(), (got, ref)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("op", [oracle.MAX, oracle.MIN])
+@pytest.mark.parametrize("exclusive", [False, True])
+@pytest.mark.parametrize("n", [5, 70_001, 3_000_017])
+def test_scan_maxmin_signed_zero_bit_exact(dt, op, exclusive, n):
+    x = zeros_heavy(dt, n, 3 * n + op)
+    got = G.scan(to_dev(x), exclusive=exclusive, op=op).cpu().numpy()
+    ref = oracle.scan(oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE, x, op=op)
+    assert np.array_equal(bits(got), bits(ref))
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_ewmap_maxmin_signed_zero_bit_exact(dt):
+    n = 100_003
+    x, y = zeros_heavy(dt, n, 21), zeros_heavy(dt, n, 22)
+    for ew, op in ((oracle.EW_MAX, G._abi.GA_EW_MAX), (oracle.EW_MIN, G._abi.GA_EW_MIN)):
+        got = G.elementwise(op, to_dev(x), to_dev(y)).cpu().numpy()
+        ref = oracle.ewmap(ew, x, y)
+        # max(NaN, NaN) is NaN on both sides; payloads compare as a class (R8)
+        assert np.array_equal(np.isnan(got), np.isnan(ref)), ew
+        keep = ~np.isnan(ref)
+        assert np.array_equal(bits(got[keep]), bits(ref[keep])), ew
