@@ -215,17 +215,16 @@ struct Op<GA_OP_SUM, T> {
   __device__ static T fold(T a, T b) { return e_add(a, b); }
 };
 // Floats: maximumNumber / minimumNumber of IEEE 754-2019 — a NaN operand
-// loses (fmaxf/fminf, R6) and -0 < +0 (the tie a == b is broken on the sign
-// bit, R7), a total order on the non-NaN values, so the result of a fold is
-// the same bits in any fold order.
-__device__ __forceinline__ bool sign_of(float a) { return __float_as_uint(a) >> 31; }
-__device__ __forceinline__ bool sign_of(double a) { return (uint64_t)__double_as_longlong(a) >> 63; }
+// loses (R6) and -0 < +0 (R7), a total order on the non-NaN values, so a
+// fold gives the same bits in any order.  sm_100a's FMNMX / DMNMX (fmaxf,
+// fminf, fmax, fmin) already order the zeros that way in both operand
+// orders (tools/lab/zero_sign_probe.cu), so no tie-break is needed here.
 template <typename T>
 struct Op<GA_OP_MAX, T> {
   __device__ static T neutral() { return Limits<T>::lowest(); }
   __device__ static T fold(T a, T b) {
-    if constexpr (std::is_same<T, float>::value) return a == b ? (sign_of(a) ? b : a) : fmaxf(a, b);
-    else if constexpr (std::is_same<T, double>::value) return a == b ? (sign_of(a) ? b : a) : fmax(a, b);
+    if constexpr (std::is_same<T, float>::value) return fmaxf(a, b);
+    else if constexpr (std::is_same<T, double>::value) return fmax(a, b);
     else return a > b ? a : b;
   }
 };
@@ -233,8 +232,8 @@ template <typename T>
 struct Op<GA_OP_MIN, T> {
   __device__ static T neutral() { return Limits<T>::highest(); }
   __device__ static T fold(T a, T b) {
-    if constexpr (std::is_same<T, float>::value) return a == b ? (sign_of(a) ? a : b) : fminf(a, b);
-    else if constexpr (std::is_same<T, double>::value) return a == b ? (sign_of(a) ? a : b) : fmin(a, b);
+    if constexpr (std::is_same<T, float>::value) return fminf(a, b);
+    else if constexpr (std::is_same<T, double>::value) return fmin(a, b);
     else return a < b ? a : b;
   }
 };
