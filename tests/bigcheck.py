@@ -120,3 +120,77 @@ def chunked_scan_compare(fetch, n, kind, seed, lo, hi, out_dtype, exclusive, chu
         shm.close()
         shm.unlink()
     return compared, mismatches, first
+
+
+def _chunk_sum_abs_job(args):
+    import oracle
+    import synth
+    kind, seed, start, m = args
+    x = synth.host_fill(kind, seed, m, start=start)
+    v, sa = oracle.reduce(oracle.SUM, oracle.MAP_ID, x, return_sumabs=True)
+    return float(v), float(sa)
+
+
+def _float_scan_cmp_job(args):
+    """One chunk of a float SUM scan against the oracle's exact prefix sums
+    within DESIGN.md R22's bound, global index i: |gpu_i - S_i| <=
+    (i/2048 + 512) * u * (sum_{j<=i} |x_j|)."""
+    from multiprocessing import shared_memory
+    import oracle
+    import synth
+    (shm_name, off, kind, seed, start, m, carry, abs_carry, exclusive, out_dtype, u) = args
+    odt = np.dtype(out_dtype)
+    shm = shared_memory.SharedMemory(name=shm_name)
+    try:
+        got = np.ndarray((m,), dtype=odt, buffer=shm.buf, offset=off).astype(np.float64)
+        x = synth.host_fill(kind, seed, m, start=start)
+        ref, sa = oracle.scan(oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE, x, carry=carry,
+                              return_sumabs=True)
+        sa_global = abs_carry + (sa - abs(carry))
+        lim = ((start + np.arange(m, dtype=np.float64)) / 2048.0 + 512.0) * u * sa_global + 1e-300
+        err = np.abs(got - ref)
+        bad = np.flatnonzero(err > lim)
+        return (start, int(bad.size), int(start + bad[0]) if bad.size else -1, float(np.max(err / lim)))
+    finally:
+        shm.close()
+
+
+def chunked_float_scan_compare(fetch, n, kind, seed, out_dtype, exclusive, chunk=CHUNK, batch=32, procs=None):
+    """Every element of a float SUM scan of n elements against the chunked
+    oracle: chunk c starts from the exact sum of the chunks before it (the
+    oracle's Neumaier float64 chunk sums combined with math.fsum), and each
+    element must lie within R22's bound.  Returns (compared, violations,
+    first violating index or -1, max error / bound)."""
+    from multiprocessing import shared_memory
+    odt = np.dtype(out_dtype)
+    u = 2.0 ** -24 if odt == np.float32 else 2.0 ** -53
+    starts = list(range(0, n, chunk))
+    procs = procs or max(1, min(len(os.sched_getaffinity(0)), 32))
+    with mp.get_context("spawn").Pool(procs) as pool:
+        parts = pool.map(_chunk_sum_abs_job, [(kind, seed, s, min(chunk, n - s)) for s in starts], chunksize=1)
+    carries, abs_carries = [], []
+    for c in range(len(starts)):
+        carries.append(math.fsum(p[0] for p in parts[:c]))
+        abs_carries.append(math.fsum(p[1] for p in parts[:c]))
+    shm = shared_memory.SharedMemory(create=True, size=batch * chunk * odt.itemsize)
+    compared, bad_total, first, worst = 0, 0, -1, 0.0
+    try:
+        with mp.get_context("spawn").Pool(procs) as pool:
+            for b0 in range(0, len(starts), batch):
+                jobs = []
+                for j, start in enumerate(starts[b0:b0 + batch]):
+                    m = min(chunk, n - start)
+                    off = j * chunk * odt.itemsize
+                    fetch(start, m, np.ndarray((m,), dtype=odt, buffer=shm.buf, offset=off))
+                    jobs.append((shm.name, off, kind, seed, start, m, carries[b0 + j], abs_carries[b0 + j], exclusive,
+                                 odt.str, u))
+                for start, bad, idx, w in pool.map(_float_scan_cmp_job, jobs, chunksize=1):
+                    compared += min(chunk, n - start)
+                    bad_total += bad
+                    worst = max(worst, w)
+                    if bad and (first < 0 or idx < first):
+                        first = idx
+    finally:
+        shm.close()
+        shm.unlink()
+    return compared, bad_total, first, worst

@@ -69,3 +69,23 @@ def test_chunked_scan_compare_finds_a_shifted_tile():
     _, bad, first = bigcheck.chunked_scan_compare(_fetch(bad_out), n, synth.I32_RANGE, 3, 0, 9, np.int32, False,
                                                   chunk=1024, batch=8, procs=2)
     assert bad == 512 and first == 5000
+
+
+@pytest.mark.parametrize("exclusive", [False, True])
+def test_chunked_float_scan_compare(exclusive):
+    """A float32 scan computed in float64 and rounded once (far inside R22's
+    bound) passes; the same with one element off by 1% of its prefix fails
+    exactly there."""
+    n, chunk = 3 * 2048 + 91, 2048
+    x = synth.host_fill(synth.F32_S11, 5, n).astype(np.float64)
+    inc = np.cumsum(x)
+    ref = (np.concatenate([[0.0], inc[:-1]]) if exclusive else inc).astype(np.float32)
+    res = bigcheck.chunked_float_scan_compare(_fetch(ref), n, synth.F32_S11, 5, np.float32, exclusive, chunk=chunk,
+                                              batch=2, procs=2)
+    assert res[:3] == (n, 0, -1) and res[3] <= 1.0 / 512  # one rounding: <= u|S_i| <= u sum|x|
+    bad = ref.copy()
+    i = 2 * 2048 + 17
+    bad[i] += np.float32(0.01 * np.sum(np.abs(x[:i + 1])) + 1.0)
+    res = bigcheck.chunked_float_scan_compare(_fetch(bad), n, synth.F32_S11, 5, np.float32, exclusive, chunk=chunk,
+                                              batch=2, procs=2)
+    assert res[1] == 1 and res[2] == i

@@ -9,7 +9,9 @@ element by element, against the chunked oracle (bigcheck.chunked_scan_compare).
   C2  fp32/fp64 axpbyz (full, bit-exact) and norm2 (tolerance) on n = 2^28
   C3  int32/int64 sum (exact), max (exact, planted), inclusive scan on n = 2^30
   C4  fp32 dot + norm2 on n = 2^33 (one GPU holds both 32 GiB inputs)
-  C5  int32 exclusive scan on n = 2^33 (every element, chunked oracle)
+  C5  int32 exclusive scan on n = 2^33 (every element, chunked oracle), also
+      as 8 contiguous shards with the sharded path's totals -> carry-in
+  float32 SUM scan at 2^28: every element within R22's bound
   bench step: axpbyz(5, x, 6, y) + dot + sum + norm2 + exclusive scan at 2^28."""
 import math
 
@@ -227,3 +229,49 @@ def test_bench_step_full_size():
     kh = synth.host_fill(synth.I32_RANGE, synth.SEED_INT, n, lo=0, hi=9)
     assert np.array_equal(s.cpu().numpy(), oracle.scan(oracle.EXCLUSIVE, kh))   # and the whole vector
     assert math.isfinite(float(r[0]))
+
+
+@pytest.mark.parametrize("exclusive", [False, True])
+def test_float_sum_scan_2p28_every_element_within_r22(exclusive):
+    """float32 SUM scan of 2^28 signed U[-1, 1) elements (the bench size):
+    every element within R22's bound of the exact prefix sum, chunk by chunk
+    (bigcheck.chunked_float_scan_compare)."""
+    n = 1 << 28
+    x = synth.device_fill(synth.F32_S11, 6, n, device=DEV)
+    out = G.scan(x, exclusive=exclusive)
+    del x
+    free()
+
+    def fetch(start, m, dest):
+        torch.from_numpy(dest).copy_(out[start:start + m])
+    compared, bad, first, worst = bigcheck.chunked_float_scan_compare(fetch, n, synth.F32_S11, 6, np.float32,
+                                                                      exclusive)
+    assert compared == n
+    assert bad == 0, f"{bad} elements outside R22, first at {first}"
+    assert worst < 1.0
+    del out
+    free()
+
+
+def test_c5_sharded_decomposition_8_shards_2p33():
+    """C5 as the 8-GPU run computes it, on one GPU: 8 contiguous shards of
+    2^30 (R16), each rank's total T_g by the reduction kernel, then each
+    shard scanned with carry-in T_0 + ... + T_{g-1} (R18, the kernels
+    gpuarray_scan_sharded runs around its allgather); the concatenated output
+    is compared whole against the unsharded chunked oracle."""
+    n, world = 1 << 33, 8
+    need_bytes(2 * n * 4)
+    k = synth.device_fill(synth.I32_RANGE, 3, n, lo=0, hi=9, device=DEV)
+    out = torch.empty_like(k)
+    totals = torch.empty(world, dtype=torch.int32, device=DEV)
+    bounds = [(g * n) // world for g in range(world + 1)]
+    for g in range(world):
+        G.sum(k[bounds[g]:bounds[g + 1]], out=totals[g:g + 1])
+    for g in range(world):  # rank g's carry: the totals of ranks < g (empty for rank 0)
+        G.scan(k[bounds[g]:bounds[g + 1]], exclusive=True, out=out[bounds[g]:bounds[g + 1]],
+               carry=totals[:g] if g else None)
+    del k
+    free()
+    _check_scan_full(out, n, synth.I32_RANGE, 3, 0, 9, np.int32, exclusive=True)
+    del out
+    free()
