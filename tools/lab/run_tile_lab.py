@@ -27,6 +27,10 @@ def main():
     lo, hi = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (18, 28)
     variants = [int(v) for v in os.environ.get("TILE_LAB_VARIANTS", "0,1,2,3,4,5,6,7,8,9,10,11,12,20,21,22,23,24").split(",")]
     L = ctypes.CDLL(LIB)
+    if os.environ.get("PERSIST_L2_MB"):
+        L.lab_set_persisting_l2.argtypes = [ctypes.c_size_t]
+        print("persisting L2 carve-out MiB:", L.lab_set_persisting_l2(int(os.environ["PERSIST_L2_MB"]) << 20),
+              flush=True)
     L.lab_scan.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                            ctypes.c_void_p]
     L.lab_scan_tile.restype = ctypes.c_int64

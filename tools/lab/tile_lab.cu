@@ -101,3 +101,11 @@ extern "C" int lab_scan_trace(int v, int64_t n, const void *in, void *out, void 
         <<<(int)p.num_tiles, 24 * 32, 0, s>>>(p, (uint64_t *)trace);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
+
+// L2 persisting carve-out (device-wide; the evict_last policy lines may live in it)
+extern "C" int lab_set_persisting_l2(size_t bytes) {
+  cudaError_t e = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes);
+  size_t got = 0;
+  cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
+  return e == cudaSuccess ? (int)(got >> 20) : -1;
+}
