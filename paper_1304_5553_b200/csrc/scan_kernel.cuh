@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "ga_device.cuh"
 
 namespace ga {
@@ -385,7 +387,17 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p,
   }
   stamp(0);
   const int64_t slice0 = tile * TILE + (int64_t)warp * ROWS * ROW;  // first element of my slice
-  const bool full = tile * TILE + TILE <= p.n;
+  // The rest of the kernel is compiled twice (L shape): for full tiles (no
+  // bounds checks at all) and for the one ragged last tile, where a lane goes
+  // scalar only if its 16 bytes straddle n (before, the whole ragged tile
+  // took scalar loads and stores and ran alone for ~16 us at the end of the
+  // scan; profiles/r2_scan.md).
+  const bool tile_full = tile * TILE + TILE <= p.n;
+  auto tile_body = [&](auto full_tag) {
+  constexpr bool full = decltype(full_tag)::value;  // false: the ragged tile (L), any tile (S, M)
+  // a lane's 16 bytes at element i may use the vector path: always in a full
+  // tile; in the L shape's ragged tile wherever they lie inside [0, n)
+  auto vec_ok = [&](int64_t i) { return tile_full || (ROWS >= 32 && i + E <= p.n); };
   const uint64_t keep = l2::policy_evict_last();
   const uint64_t drop = l2::policy_evict_first();
 
@@ -394,11 +406,17 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p,
   // the 8-byte and widened scans hold no more live state than int32.
   auto load_raw = [&](int r, uint64_t pol) -> uint4 {
     const int64_t i = slice0 + (int64_t)r * ROW + lane * E;
-    if (full) return l2::ldg128_hint<NC>(p.in + i, pol);
-    Tin e[E];  // ragged tail: padding only reaches positions >= n (never stored)
+    // the ragged last tile takes the vector path too wherever a lane's 16
+    // bytes lie inside [0, n): only the lane straddling n goes scalar
+    if constexpr (full) {
+      return l2::ldg128_hint<NC>(p.in + i, pol);
+    } else {
+      if (vec_ok(i)) return l2::ldg128_hint<NC>(p.in + i, pol);
+      Tin e[E];  // padding only reaches positions >= n (never stored)
 #pragma unroll
-    for (int k = 0; k < E; ++k) e[k] = i + k < p.n ? p.in[i + k] : Op<OP, Tin>::neutral();
-    return Chunk<Tin>::pack(e);
+      for (int k = 0; k < E; ++k) e[k] = i + k < p.n ? p.in[i + k] : Op<OP, Tin>::neutral();
+      return Chunk<Tin>::pack(e);
+    }
   };
   auto widen = [&](const uint4 &raw, T (&v)[E]) {
     Tin e[E];
@@ -497,7 +515,9 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p,
         else o[k] = O::fold(cb, v[k]);
       }
       const int64_t i = slice0 + (int64_t)(r0 + u) * ROW + lane * E;
-      if (full) {
+      bool vec = true;
+      if constexpr (!full) vec = vec_ok(i);
+      if (vec) {
         if constexpr (WIDEN) {
           const T lo[2] = {o[0], o[1]}, hi[2] = {o[2], o[3]};
           l2::stg256_hint(p.out + i, Chunk<T>::pack(lo), Chunk<T>::pack(hi), drop);
@@ -529,6 +549,11 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p,
     base = O::fold(base, ctot);
   }
   stamp(3);
+  };
+  // the split pays off for the long L-shape tiles; the short S/M ones keep one
+  // (bounds-checked) body, which keeps them inside 64 registers
+  if (ROWS >= 32 && tile_full) tile_body(std::integral_constant<bool, ROWS >= 32>{});
+  else tile_body(std::false_type{});
 }
 
 // ===========================================================================
