@@ -551,6 +551,7 @@ def main():
             "gpu_launches": int(launches), "launches_per_step": launches / args.steps, "clocks": clk,
             "collective": ("none (single GPU)" if world == 1 else
                            "fused in-kernel NVLink finish" if xch is not None else
+                           "gloo via torch.distributed (BENCH_SHARE_GPU test mode: ranks share one GPU)" if share else
                            "NCCL inside gpuarray_reduce_sharded / gpuarray_scan_sharded"),
         }
         if extras is not None:
