@@ -2,7 +2,7 @@
 L-shape int32 exclusive kernel compiled with TRACE (tile_lab.cu
 lab_scan_trace), one traced call at 2^28 after warm-up, with (0) and
 without (1) the L2 prefetch.  Results: profiles/r2_scan.md.
-    python tools/lab/trace_l2.py run | analyze"""
+    [TRACE_LOG2N=k] python tools/lab/trace_l2.py run | analyze"""
 import ctypes
 import os
 import sys
@@ -20,7 +20,7 @@ def run():
     L = ctypes.CDLL(os.environ.get("TILE_LAB_LIB", os.path.join(HERE, "libtile_lab.so")))
     L.lab_scan_trace.argtypes = [ctypes.c_int, ctypes.c_int64] + [ctypes.c_void_p] * 5
     dev = torch.device("cuda:0")
-    n = 1 << 28
+    n = 1 << int(os.environ.get("TRACE_LOG2N", "28"))
     k = torch.randint(0, 10, (n,), dtype=torch.int32, device=dev)
     o = torch.empty_like(k)
     ws = torch.zeros(1 << 22, dtype=torch.uint8, device=dev)
