@@ -54,7 +54,7 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 // DW data warps (+1 look-back warp), SLICE input bytes per data warp (a
 // multiple of 512: SLICE/512 rows of 32 lanes x 16 bytes).
 template <int OP, typename T, int DW, int SLICE, int DEPTH, bool NC, bool EXCLUSIVE, bool PF, bool TRACE = false,
-          bool STMA = false>
+          bool STMA = false, bool SRV = false>
 __global__ void __launch_bounds__((DW + 1) * 32) scan_smem_kernel(ScanArgs<T, T> p, uint64_t *trace = nullptr) {
   using O = Op<OP, T>;
   constexpr int E = Chunk<T>::E;        // elements per lane per row
@@ -136,6 +136,26 @@ __global__ void __launch_bounds__((DW + 1) * 32) scan_smem_kernel(ScanArgs<T, T>
       prefix = lane == 0 ? carry_in<OP, T>(p) : neutral;
       prefix = __shfl_sync(0xffffffffu, prefix, 0);
       if (lane == 0) p.status.publish(0, epoch, FLAG_INCLUSIVE, O::fold(prefix, total));
+    } else if constexpr (SRV) {
+      // prefix server (tile 0's CTA, below) publishes every tile's INCLUSIVE
+      // in order: publish the AGGREGATE, then wait for the predecessor's
+      // INCLUSIVE — one status word, polled by lane 0
+      if (lane == 0) p.status.publish(tile, epoch, FLAG_AGGREGATE, total);
+      if (TRACE && lane == 0) stamp(2);
+      T pv = neutral;
+      if (lane == 0) {
+        uint32_t f, spins = 0;
+        uint64_t t0 = 0;
+        while ((f = p.status.read(tile - 1, epoch, pv)) != FLAG_INCLUSIVE) {
+          if ((++spins & 1023u) == 0) {
+            const uint64_t now = globaltimer_ns();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 5000000000ull) __trap();  // lab guard: never hang the box
+          }
+        }
+      }
+      prefix = __shfl_sync(0xffffffffu, pv, 0);
+      if (TRACE && lane == 0) stamp(3);
     } else {
       if (lane == 0) p.status.publish(tile, epoch, FLAG_AGGREGATE, total);
       if (TRACE && lane == 0) stamp(2);
@@ -173,7 +193,40 @@ __global__ void __launch_bounds__((DW + 1) * 32) scan_smem_kernel(ScanArgs<T, T>
     }
   }
   __syncthreads();
-  if (warp == DW) return;
+  if (warp == DW) {
+    if constexpr (SRV) {
+      if (tile == 0) {
+        // The prefix server: a sliding window of 32 tiles; every poll takes
+        // the run of consecutive published AGGREGATEs from the window start,
+        // scans it onto the running prefix and publishes their INCLUSIVEs.
+        T run = neutral;
+        if (lane == 0) {
+          T v0;
+          p.status.read(0, epoch, v0);
+          run = v0;
+        }
+        run = __shfl_sync(0xffffffffu, run, 0);
+        int64_t next = 1;
+        const int64_t last = p.num_tiles - 1;  // nobody needs the last tile's INCLUSIVE
+        uint64_t t0 = globaltimer_ns();
+        while (next < last) {
+          if (globaltimer_ns() - t0 > 5000000000ull) __trap();  // lab guard: never hang the box
+          const int64_t t = next + lane;
+          T v = neutral;
+          uint32_t f = FLAG_INVALID;
+          if (t < last) f = p.status.read(t, epoch, v);
+          const uint32_t ready = __ballot_sync(0xffffffffu, t < last && f != FLAG_INVALID);
+          const int cnt = __ffs(~ready) - 1 < 0 ? 32 : __ffs(~ready) - 1;  // leading ready lanes
+          if (cnt == 0) continue;
+          const T x = warp_inclusive<OP, T>(lane < cnt ? v : neutral, lane);
+          if (lane < cnt) p.status.publish(t, epoch, FLAG_INCLUSIVE, O::fold(run, x));
+          run = O::fold(run, __shfl_sync(0xffffffffu, x, cnt - 1));
+          next += cnt;
+        }
+      }
+    }
+    return;
+  }
 
   // phase 3: add the slice prefix and store
   const T base = s_slice[warp];

@@ -7,11 +7,11 @@
 
 using namespace ga::scan_detail;
 
-template <typename T, int DW, int SLICE, int D, bool EX, bool PF, bool STMA = false>
+template <typename T, int DW, int SLICE, int D, bool EX, bool PF, bool STMA = false, bool SRV = false>
 static int run(int64_t n, const void *in, void *out, void *ws, int pfd, cudaStream_t s) {
   constexpr int64_t TILE = (int64_t)DW * SLICE / sizeof(T);
   constexpr int SMEM = DW * SLICE;
-  auto k = scan_smem_kernel<GA_OP_SUM, T, DW, SLICE, D, true, EX, PF, false, STMA>;
+  auto k = scan_smem_kernel<GA_OP_SUM, T, DW, SLICE, D, true, EX, PF, false, STMA, SRV>;
   static bool init = false;
   if (!init) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -32,6 +32,14 @@ static int run(int64_t n, const void *in, void *out, void *ws, int pfd, cudaStre
   X(33, int32_t, 8, 12288, true)          \
   X(34, int32_t, 16, 4096, false)         \
   X(35, int32_t, 8, 4096, false)
+
+#define VSRV(X)                           \
+  X(60, int32_t, 8, 12288, false)         \
+  X(61, int32_t, 8, 8192, false)          \
+  X(62, int32_t, 8, 12288, true)          \
+  X(63, int32_t, 8, 8192, true)           \
+  X(64, int32_t, 16, 6144, true)          \
+  X(65, int32_t, 8, 4096, true)
 
 #define V(X)                              \
   X(0, int32_t, 8, 8192, false)           \
@@ -61,6 +69,10 @@ extern "C" int smem_lab(int v, int ex, int64_t n, const void *in, void *out, voi
 #define C(id, T, DW, SL, PF) \
   case id: return ex ? run<T, DW, SL, 8, true, PF, true>(n, in, out, ws, pfd, s) : run<T, DW, SL, 8, false, PF, true>(n, in, out, ws, pfd, s);
     VS(C)
+#undef C
+#define C(id, T, DW, SL, PF) \
+  case id: return ex ? run<T, DW, SL, 8, true, PF, false, true>(n, in, out, ws, pfd, s) : run<T, DW, SL, 8, false, PF, false, true>(n, in, out, ws, pfd, s);
+    VSRV(C)
 #undef C
   }
   return 2;
