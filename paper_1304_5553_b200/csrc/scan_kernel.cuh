@@ -314,6 +314,28 @@ __device__ __forceinline__ void stg256_hint(void *p, const uint4 &a, const uint4
                "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w), "l"(pol)
                : "memory");
 }
+template <bool NC>
+__device__ __forceinline__ V32 ldg256_hint(const void *p, uint64_t pol) {
+  V32 v;
+  if constexpr (NC)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=r"(v.r[0]), "=r"(v.r[1]), "=r"(v.r[2]), "=r"(v.r[3]), "=r"(v.r[4]), "=r"(v.r[5]), "=r"(v.r[6]),
+                   "=r"(v.r[7])
+                 : "l"(p), "l"(pol));
+  else
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=r"(v.r[0]), "=r"(v.r[1]), "=r"(v.r[2]), "=r"(v.r[3]), "=r"(v.r[4]), "=r"(v.r[5]), "=r"(v.r[6]),
+                   "=r"(v.r[7])
+                 : "l"(p), "l"(pol)
+                 : "memory");
+  return v;
+}
+__device__ __forceinline__ void stg256v_hint(void *p, const V32 &v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(p),
+               "r"(v.r[0]), "r"(v.r[1]), "r"(v.r[2]), "r"(v.r[3]), "r"(v.r[4]), "r"(v.r[5]), "r"(v.r[6]), "r"(v.r[7]),
+               "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void stg128_hint(void *p, const uint4 &v, uint64_t pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
@@ -346,12 +368,18 @@ __device__ __forceinline__ void draw_tile(const A &p, uint32_t &tile, uint32_t &
 // P1U: rows in flight per warp in phase 1 (its only live state is the raw
 // rows, so it can exceed phase 3's UNROLL).
 template <int OP, typename T, typename Tin, int WARPS, int ROWS, int UNROLL, int DEPTH, bool NC, bool EXCLUSIVE,
-          bool EARLY, int P1U = UNROLL, int PF_ROWS = 0, bool TRACE = false>
+          bool EARLY, int P1U = UNROLL, int PF_ROWS = 0, bool TRACE = false, int RB = 512>
 __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p, uint64_t *trace) {
   pdl_enter();
   using O = Op<OP, T>;
-  constexpr int E = Chunk<Tin>::E;  // elements per lane per row
-  constexpr int ROW = 32 * E;       // elements per row: 512 bytes of input
+  // RB: input bytes per warp row — 512 (16 bytes per lane, LDG/STG.128) or
+  // 1024 (32 bytes per lane, LDG/STG.256: half the memory instructions and
+  // one warp scan per 8 elements per lane instead of per 4)
+  static_assert(RB == 512 || RB == 1024, "row bytes");
+  using Raw = std::conditional_t<RB == 1024, V32, uint4>;
+  constexpr int E = RB / 32 / (int)sizeof(Tin);  // elements per lane per row
+  constexpr int ROW = 32 * E;                     // elements per row
+  constexpr bool LONG = ROWS * RB >= 16384;       // the L shape's 16 KiB slices (full / ragged bodies split)
   constexpr bool WIDEN = sizeof(T) != sizeof(Tin);
   static_assert(!WIDEN || (sizeof(T) == 8 && sizeof(Tin) == 4), "widening is 4 -> 8 bytes");
   constexpr int64_t TILE = (int64_t)WARPS * ROWS * ROW;
@@ -397,39 +425,58 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p,
   constexpr bool full = decltype(full_tag)::value;  // false: the ragged tile (L), any tile (S, M)
   // a lane's 16 bytes at element i may use the vector path: always in a full
   // tile; in the L shape's ragged tile wherever they lie inside [0, n)
-  auto vec_ok = [&](int64_t i) { return tile_full || (ROWS >= 32 && i + E <= p.n); };
+  auto vec_ok = [&](int64_t i) { return tile_full || (LONG && i + E <= p.n); };
   const uint64_t keep = l2::policy_evict_last();
   const uint64_t drop = l2::policy_evict_first();
 
   // A row stays in registers as its raw 16 input bytes (4 registers for
   // every T / Tin); it is unpacked and widened only where it is folded, so
   // the 8-byte and widened scans hold no more live state than int32.
-  auto load_raw = [&](int r, uint64_t pol) -> uint4 {
-    const int64_t i = slice0 + (int64_t)r * ROW + lane * E;
-    // the ragged last tile takes the vector path too wherever a lane's 16
-    // bytes lie inside [0, n): only the lane straddling n goes scalar
-    if constexpr (full) {
-      return l2::ldg128_hint<NC>(p.in + i, pol);
-    } else {
-      if (vec_ok(i)) return l2::ldg128_hint<NC>(p.in + i, pol);
-      Tin e[E];  // padding only reaches positions >= n (never stored)
+  auto ldv = [&](const Tin *a, uint64_t pol) -> Raw {
+    if constexpr (RB == 1024) return l2::ldg256_hint<NC>(a, pol);
+    else return l2::ldg128_hint<NC>(a, pol);
+  };
+  auto pack_in = [&](const Tin (&e)[E]) -> Raw {
+    if constexpr (RB == 1024) {
+      V32 w;
 #pragma unroll
-      for (int k = 0; k < E; ++k) e[k] = i + k < p.n ? p.in[i + k] : Op<OP, Tin>::neutral();
+      for (int k = 0; k < E; ++k) vset<Tin>(w, k, e[k]);
+      return w;
+    } else {
       return Chunk<Tin>::pack(e);
     }
   };
-  auto widen = [&](const uint4 &raw, T (&v)[E]) {
-    Tin e[E];
-    Chunk<Tin>::unpack(raw, e);
+  auto load_raw = [&](int r, uint64_t pol) -> Raw {
+    const int64_t i = slice0 + (int64_t)r * ROW + lane * E;
+    // the ragged last tile takes the vector path too wherever a lane's
+    // bytes lie inside [0, n): only the lane straddling n goes scalar
+    if constexpr (full) {
+      return ldv(p.in + i, pol);
+    } else {
+      if (vec_ok(i)) return ldv(p.in + i, pol);
+      Tin e[E];  // padding only reaches positions >= n (never stored)
 #pragma unroll
-    for (int k = 0; k < E; ++k) v[k] = (T)e[k];
+      for (int k = 0; k < E; ++k) e[k] = i + k < p.n ? p.in[i + k] : Op<OP, Tin>::neutral();
+      return pack_in(e);
+    }
+  };
+  auto widen = [&](const Raw &raw, T (&v)[E]) {
+    if constexpr (RB == 1024) {
+#pragma unroll
+      for (int k = 0; k < E; ++k) v[k] = (T)vget<Tin>(raw, k);
+    } else {
+      Tin e[E];
+      Chunk<Tin>::unpack(raw, e);
+#pragma unroll
+      for (int k = 0; k < E; ++k) v[k] = (T)e[k];
+    }
   };
 
   // phase 1: slice folds
   T acc = neutral;
 #pragma unroll 1
   for (int r0 = 0; r0 < ROWS; r0 += P1U) {
-    uint4 raw[P1U];
+    Raw raw[P1U];
 #pragma unroll
     for (int u = 0; u < P1U; ++u) raw[u] = load_raw(r0 + u, keep);
 #pragma unroll
@@ -456,7 +503,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p,
     if (p.pf_dist > 0 && lane == 0 && (nt + 1) * TILE <= p.n) {
       const Tin *a = p.in + nt * TILE + (int64_t)warp * ROWS * ROW;
       asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a),
-                   "r"((uint32_t)(PF_ROWS * 512)), "l"(keep)
+                   "r"((uint32_t)(PF_ROWS * RB)), "l"(keep)
                    : "memory");
     }
   }
@@ -486,7 +533,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p,
   // warp-exclusive scan of the lanes' in-lane folds) and the chunk fold
   // (ctot).  store_chunk redoes the in-lane running fold v0 ⊕ .. ⊕ vk — the
   // same operations in the same order, so results do not change.
-  auto load_local = [&](int r0, uint4 (&raw)[UNROLL], T (&off)[UNROLL], T &ctot) {
+  auto load_local = [&](int r0, Raw (&raw)[UNROLL], T (&off)[UNROLL], T &ctot) {
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) raw[u] = load_raw(r0 + u, drop);
     ctot = neutral;
@@ -501,7 +548,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p,
       ctot = O::fold(ctot, __shfl_sync(0xffffffffu, x, 31));
     }
   };
-  auto store_chunk = [&](int r0, const uint4 (&raw)[UNROLL], const T (&off)[UNROLL], T base) {
+  auto store_chunk = [&](int r0, const Raw (&raw)[UNROLL], const T (&off)[UNROLL], T base) {
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
       const T cb = O::fold(base, off[u]);
@@ -518,11 +565,18 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p,
       bool vec = true;
       if constexpr (!full) vec = vec_ok(i);
       if (vec) {
-        if constexpr (WIDEN) {
-          const T lo[2] = {o[0], o[1]}, hi[2] = {o[2], o[3]};
-          l2::stg256_hint(p.out + i, Chunk<T>::pack(lo), Chunk<T>::pack(hi), drop);
-        } else {
+        constexpr int OB = E * (int)sizeof(T);  // output bytes per lane: 16, 32 or 64
+        if constexpr (OB == 16) {
           l2::stg128_hint(p.out + i, Chunk<T>::pack(o), drop);
+        } else {
+          constexpr int EPV = 32 / (int)sizeof(T);
+#pragma unroll
+          for (int h = 0; h < OB / 32; ++h) {
+            V32 w;
+#pragma unroll
+            for (int k = 0; k < EPV; ++k) vset<T>(w, k, o[h * EPV + k]);
+            l2::stg256v_hint(p.out + i + h * EPV, w, drop);
+          }
         }
       } else {
 #pragma unroll
@@ -531,7 +585,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p,
       }
     }
   };
-  uint4 v0[UNROLL];
+  Raw v0[UNROLL];
   T off0[UNROLL], ctot0;
   const bool early = EARLY && warp != 0;
   if (early) load_local(0, v0, off0, ctot0);
@@ -542,7 +596,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p,
   base = O::fold(base, ctot0);
 #pragma unroll 1
   for (int r0 = UNROLL; r0 < ROWS; r0 += UNROLL) {
-    uint4 v[UNROLL];
+    Raw v[UNROLL];
     T off[UNROLL], ctot;
     load_local(r0, v, off, ctot);
     store_chunk(r0, v, off, base);
@@ -552,7 +606,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p,
   };
   // the split pays off for the long L-shape tiles; the short S/M ones keep one
   // (bounds-checked) body, which keeps them inside 64 registers
-  if (ROWS >= 32 && tile_full) tile_body(std::integral_constant<bool, ROWS >= 32>{});
+  if (LONG && tile_full) tile_body(std::integral_constant<bool, LONG>{});
   else tile_body(std::false_type{});
 }
 

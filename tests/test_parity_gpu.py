@@ -670,3 +670,26 @@ def test_ewmap_maxmin_signed_zero_bit_exact(dt):
         assert np.array_equal(np.isnan(got), np.isnan(ref)), ew
         keep = ~np.isnan(ref)
         assert np.array_equal(bits(got[keep]), bits(ref[keep])), ew
+
+
+@pytest.mark.parametrize("dt", [np.int64, np.float64])
+@pytest.mark.parametrize("offset", [0, 2])
+def test_scan_8byte_l_shape_both_row_widths(dt, offset):
+    """8-byte scans at the L shape take 1 KiB rows (LDG/STG.256) when input and
+    output are 32-byte aligned, else 512-byte rows: a view 2 elements (16
+    bytes) into an allocation exercises the second path.  Integer scans are
+    exact; float64 SUM within R22."""
+    n = 256 * 24 * 32 * 64 + 12345  # >= 256 L tiles, ragged last tile
+    if dt == np.int64:
+        x = np.random.default_rng(offset + 5).integers(-(1 << 40), 1 << 40, size=n, dtype=np.int64)
+    else:
+        x = host_data(dt, n, 9, signed=True)
+    for exclusive in (False, True):
+        kind = oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE
+        got = G.scan(to_dev(x, offset), exclusive=exclusive).cpu().numpy()
+        if dt == np.int64:
+            assert np.array_equal(got, oracle.scan(kind, x))
+        else:
+            ref, sa = oracle.scan(kind, x, return_sumabs=True)
+            d = np.arange(n) / 2048.0 + 512
+            assert np.all(np.abs(got - ref) <= d * 2.0 ** -53 * sa + 1e-300)

@@ -59,7 +59,7 @@ def test_elementwise_float_has_no_fma(sass):
 
 
 def test_vector_widths(sass):
-    seen = {"ew": False, "red": False, "scan": False}
+    seen = {"ew": False, "red": False, "scan": False, "scan1k": False}
     for name, body in sass.items():
         d = demangled_kind(name)
         if "ew_vec_kernel" in d:
@@ -70,8 +70,12 @@ def test_vector_widths(sass):
             seen["red"] = True
         if "scan_l2_kernel" in d:
             widen = "ScanArgs<double, float>" in d or "ScanArgs<long, int>" in d
-            st = r"STG\.E\S*\.256" if widen else r"STG\.E\S*\.128"  # widened rows: 32 B per lane
-            assert re.search(r"LDG\.E\S*\.128", body) and re.search(st, body), d
+            if ", 1024>" in d:  # 1 KiB rows (8-byte L-shape scans): 32 B per lane each way
+                assert re.search(r"LDG\.E\S*\.256", body) and re.search(r"STG\.E\S*\.256", body), d
+                seen["scan1k"] = True
+            else:
+                st = r"STG\.E\S*\.256" if widen else r"STG\.E\S*\.128"  # widened rows: 32 B per lane
+                assert re.search(r"LDG\.E\S*\.128", body) and re.search(st, body), d
             seen["scan"] = True
     assert all(seen.values()), seen
 

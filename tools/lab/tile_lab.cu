@@ -60,9 +60,29 @@ static int run(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   X(50, int64_t, 24, 32, 32, 42, 4, 4, 16)        \
   X(51, int64_t, 24, 32, 32, 42, 4, 8, 8)
 
+// 1 KiB rows (RB = 1024: LDG/STG.256): T, warps, rows, UNROLL, P1U, PF rows, distance
+template <typename T, int W, int R, int U, int P1, int PF, int DIST, bool EX = true>
+static int run_rb(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
+  constexpr int64_t TILE = (int64_t)W * R * 1024 / sizeof(T);
+  constexpr int D = sizeof(T) == 8 ? 4 : 8;
+  ScanArgs<T> p = make_args<T>(n, TILE, in, out, nullptr, 0, ws);
+  p.pf_dist = DIST;
+  scan_l2_kernel<GA_OP_SUM, T, T, W, R, U, D, true, EX, true, P1, PF, false, 1024>
+      <<<(int)p.num_tiles, W * 32, 0, s>>>(p, nullptr);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
 extern "C" int lab_scan(int v, int64_t n, const void *in, void *out, void *ws, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
   switch (v) {
+    case 140: return run_rb<int32_t, 24, 16, 4, 4, 16, 42>(n, in, out, ws, s);
+    case 141: return run_rb<int32_t, 24, 16, 4, 8, 16, 42>(n, in, out, ws, s);
+    case 142: return run_rb<int32_t, 24, 16, 2, 4, 16, 42>(n, in, out, ws, s);
+    case 143: return run_rb<int32_t, 24, 16, 4, 4, 16, 60>(n, in, out, ws, s);
+    case 144: return run_rb<int32_t, 24, 16, 4, 4, 16, 30>(n, in, out, ws, s);
+    case 145: return run_rb<int32_t, 24, 16, 4, 4, 16, 42, false>(n, in, out, ws, s);
+    case 146: return run_rb<int64_t, 24, 16, 2, 4, 16, 42>(n, in, out, ws, s);
+    case 147: return run_rb<int64_t, 24, 16, 4, 4, 16, 42>(n, in, out, ws, s);
 #define C(id, T, W, R, U, D, P) case id: return run<T, W, R, U, D, P>(n, in, out, ws, s);
     V(C)
 #undef C
@@ -74,6 +94,14 @@ extern "C" int lab_scan(int v, int64_t n, const void *in, void *out, void *ws, v
 }
 extern "C" int64_t lab_scan_tile(int v) {
   switch (v) {
+    case 140:
+    case 141:
+    case 142:
+    case 143:
+    case 144:
+    case 145: return 24 * 16 * 256;
+    case 146:
+    case 147: return 24 * 16 * 128;
 #define C(id, T, W, R, U, D, P) case id: return (int64_t)W * R * 512 / sizeof(T);
     V(C)
 #undef C
@@ -83,7 +111,7 @@ extern "C" int64_t lab_scan_tile(int v) {
   }
   return 0;
 }
-extern "C" int lab_scan_elem_bytes(int v) { return ((v >= 20 && v < 30) || v == 46 || v >= 50) ? 8 : 4; }
+extern "C" int lab_scan_elem_bytes(int v) { return ((v >= 20 && v < 30) || v == 46 || (v >= 50 && v < 140) || v == 146 || v == 147) ? 8 : 4; }
 
 // the product configuration (L shape, int32, exclusive, 32 rows prefetched 42
 // ids ahead; v == 1: no prefetch) compiled with TRACE: per tile {start,
