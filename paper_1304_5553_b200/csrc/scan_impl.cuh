@@ -93,17 +93,21 @@ ga_status_t run(int64_t n, const void *in, void *out, const void *carry, int64_t
     if (PF) p.pf_dist = std::max<int64_t>(1, (int64_t)sm_count() * 2 / 7);
     // 8-byte scans at the L shape: 1 KiB rows (LDG/STG.256, 4 elements per
     // lane per row: half the memory instructions and half the shuffles of
-    // the 512-byte rows) when both arrays are 32-byte aligned — 4-5% faster
-    // at 2^28-2^30 (profiles/r2_scan.md); same tile, so the same workspace
-    if constexpr (SHAPE == SHAPE_L && sizeof(T) == 8 && sizeof(Tin) == 8) {
+    // the 512-byte rows) when both arrays are 32-byte aligned — 2-5% faster
+    // at 2^28-2^30 (profiles/r2_scan.md); same tile, so the same workspace.
+    // Widened scans (4-byte in, 8-byte scan) likewise take 1 KiB input rows
+    // (2 rows in flight per warp in phase 3, no prefetch): 7-8% faster at
+    // 2^28-2^30 (tools/lab/run_wide_lab.py).
+    if constexpr (SHAPE == SHAPE_L && sizeof(T) == 8) {
       if ((((uintptr_t)in | (uintptr_t)out) & 31) == 0) {
-        constexpr int R2 = R / 2, U2 = 4, P2 = 4;
+        constexpr bool WIDE = sizeof(Tin) == 4;
+        constexpr int R2 = R / 2, U2 = WIDE ? 2 : 4, P2 = 4, PF2 = WIDE ? 0 : R2;
         if (in == out)
-          launch(scan_l2_kernel<OP, T, Tin, W, R2, U2, D, false, EXCLUSIVE, true, P2, R2, false, 1024>, grid, W * 32, 0,
-                 s, p, (uint64_t *)nullptr);
+          launch(scan_l2_kernel<OP, T, Tin, W, R2, U2, D, false, EXCLUSIVE, true, P2, PF2, false, 1024>, grid, W * 32,
+                 0, s, p, (uint64_t *)nullptr);
         else
-          launch(scan_l2_kernel<OP, T, Tin, W, R2, U2, D, true, EXCLUSIVE, true, P2, R2, false, 1024>, grid, W * 32, 0,
-                 s, p, (uint64_t *)nullptr);
+          launch(scan_l2_kernel<OP, T, Tin, W, R2, U2, D, true, EXCLUSIVE, true, P2, PF2, false, 1024>, grid, W * 32,
+                 0, s, p, (uint64_t *)nullptr);
         count_launch();
         return check_launch("scan_kernel");
       }

@@ -72,6 +72,26 @@ static int run_rb(int64_t n, const void *in, void *out, void *ws, cudaStream_t s
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
+// widened int32 -> int64 with RB = 512 (product shape) or 1024
+template <int RB, int R, int U, int P1>
+static int run_wide(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
+  constexpr int64_t TILE = 24 * 32 * 512 / 4;
+  ScanArgs<int64_t, int32_t> p = make_args<int64_t, int32_t>(n, TILE, in, out, nullptr, 0, ws);
+  scan_l2_kernel<GA_OP_SUM, int64_t, int32_t, 24, R, U, 4, true, true, true, P1, 0, false, RB>
+      <<<(int)p.num_tiles, 24 * 32, 0, s>>>(p, nullptr);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+extern "C" int lab_scan_wide(int v, int64_t n, const void *in, void *out, void *ws, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (v) {
+    case 0: return run_wide<512, 32, 2, 8>(n, in, out, ws, s);
+    case 1: return run_wide<1024, 16, 2, 4>(n, in, out, ws, s);
+    case 2: return run_wide<1024, 16, 1, 4>(n, in, out, ws, s);
+    case 3: return run_wide<1024, 16, 2, 2>(n, in, out, ws, s);
+  }
+  return 2;
+}
+
 extern "C" int lab_scan(int v, int64_t n, const void *in, void *out, void *ws, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
   switch (v) {
