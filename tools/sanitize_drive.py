@@ -79,9 +79,18 @@ for n in (129 * 16384 - 3, 300 * 16384 + 5):
 
 # L-shape scans (>= 256 super-tiles: the look-back L2 prefetch of the tile 42
 # ids ahead is active), in place and out of place, plus a ragged tail
-for n, dt in ((256 * 98304 + 12345, torch.int32), (256 * 49152 + 777, torch.int64)):
-    x = arr(n, dt)
-    G.scan(x)
-    G.scan(x, exclusive=True, out=x)
+# (8-byte and widened L-shape scans read 1 KiB rows when 32-byte aligned and
+# 512-byte rows otherwise: both, via a 2-element (16-byte) view offset)
+for n, dt in ((256 * 98304 + 12345, torch.int32), (256 * 49152 + 777, torch.int64),
+              (256 * 49152 + 999, torch.float64)):
+    for off in (0, 2):
+        x = arr(n, dt, off)
+        G.scan(x)
+        G.scan(x, exclusive=True, out=x)
+        torch.cuda.synchronize()
+for dt, wide in ((torch.int32, torch.int64), (torch.float32, torch.float64)):
+    x = arr(256 * 98304 + 4321, dt)
+    G.scan(x, out_dtype=wide)
+    G.scan(x, out_dtype=wide, exclusive=True)
     torch.cuda.synchronize()
 print("drive ok", G.launch_count(), "launches")
