@@ -693,3 +693,17 @@ def test_scan_8byte_l_shape_both_row_widths(dt, offset):
             ref, sa = oracle.scan(kind, x, return_sumabs=True)
             d = np.arange(n) / 2048.0 + 512
             assert np.all(np.abs(got - ref) <= d * 2.0 ** -53 * sa + 1e-300)
+
+
+@pytest.mark.parametrize("offset", [0, 2])
+def test_scan_int64_l_shape_in_place(offset):
+    """In-place int64 scans at the L shape, 1 KiB rows (offset 0) and
+    512-byte rows (offset 2 elements = 16 bytes): coherent loads (the output
+    overwrites the input) on both row widths."""
+    n = 300 * 24 * 32 * 64 + 4097
+    x = np.random.default_rng(77 + offset).integers(-(1 << 40), 1 << 40, size=n, dtype=np.int64)
+    for exclusive in (False, True):
+        d = to_dev(x, offset)
+        G.scan(d, exclusive=exclusive, out=d)
+        ref = oracle.scan(oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE, x)
+        assert np.array_equal(d.cpu().numpy(), ref)
