@@ -18,7 +18,10 @@
 //     the other warps already load and locally scan their first 8 rows;
 //   - phase 3 re-reads the slice (L2 hit, evict_first), scans it row by row
 //     (in-chunk serial scan + warp shuffle scan) and stores 512 B per warp
-//     instruction.
+//     instruction (1 KiB rows — 32 bytes per lane — for the 8-byte and
+//     widened scans when the arrays are 32-byte aligned);
+//   - the ragged last tile has its own compiled body (vector accesses except
+//     for the one lane straddling n).
 // Look-back status words carry the call's epoch in every 64-bit word (for
 // every element size, so one workspace may serve scans of any dtype, size and
 // shape), so the workspace is zeroed once and never again (until the 30-bit

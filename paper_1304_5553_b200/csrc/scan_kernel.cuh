@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p,
   using O = Op<OP, T>;
   // RB: input bytes per warp row — 512 (16 bytes per lane, LDG/STG.128) or
   // 1024 (32 bytes per lane, LDG/STG.256: half the memory instructions and
-  // one warp scan per 8 elements per lane instead of per 4)
+  // half the warp scans per element; used for the 8-byte and widened L shapes)
   static_assert(RB == 512 || RB == 1024, "row bytes");
   using Raw = std::conditional_t<RB == 1024, V32, uint4>;
   constexpr int E = RB / 32 / (int)sizeof(Tin);  // elements per lane per row
@@ -429,9 +429,10 @@ __global__ void __launch_bounds__(WARPS * 32) scan_l2_kernel(ScanArgs<T, Tin> p,
   const uint64_t keep = l2::policy_evict_last();
   const uint64_t drop = l2::policy_evict_first();
 
-  // A row stays in registers as its raw 16 input bytes (4 registers for
-  // every T / Tin); it is unpacked and widened only where it is folded, so
-  // the 8-byte and widened scans hold no more live state than int32.
+  // A row stays in registers as its raw RB/32 input bytes per lane (4 or 8
+  // registers for every T / Tin); it is unpacked and widened only where it is
+  // folded, so the 8-byte and widened scans hold no more live state than
+  // int32 at the same row width.
   auto ldv = [&](const Tin *a, uint64_t pol) -> Raw {
     if constexpr (RB == 1024) return l2::ldg256_hint<NC>(a, pol);
     else return l2::ldg128_hint<NC>(a, pol);
