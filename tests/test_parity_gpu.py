@@ -707,3 +707,20 @@ def test_scan_int64_l_shape_in_place(offset):
         G.scan(d, exclusive=exclusive, out=d)
         ref = oracle.scan(oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE, x)
         assert np.array_equal(d.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("dt", [np.int64, np.float64])
+@pytest.mark.parametrize("op", [oracle.MAX, oracle.MIN])
+def test_scan_maxmin_8byte_l_shape(dt, op):
+    """MAX / MIN scans of 8-byte types at the L shape (1 KiB rows), inclusive
+    and exclusive, bit-exact — float64 data zero- and NaN-heavy (R6, R7)."""
+    n = 256 * 24 * 32 * 64 + 999
+    if dt == np.int64:
+        x = np.random.default_rng(op + 3).integers(-(1 << 62), 1 << 62, size=n, dtype=np.int64)
+    else:
+        x = zeros_heavy(dt, n, op + 4)
+        x[np.random.default_rng(op).integers(0, n, size=64)] = np.random.default_rng(1).standard_normal(64)
+    for exclusive in (False, True):
+        got = G.scan(to_dev(x), exclusive=exclusive, op=op).cpu().numpy()
+        ref = oracle.scan(oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE, x, op=op)
+        assert np.array_equal(bits(got), bits(ref))
