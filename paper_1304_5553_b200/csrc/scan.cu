@@ -29,9 +29,13 @@
 // id resets the counter.
 // Tile 0's exclusive prefix is the carry-in c = sum(carry[0..carry_count)),
 // which is how a sharded scan injects the totals of earlier shards.
+// Mid-size arrays (48 MiB .. 384 MiB of 4-byte input, .. 768 MiB of 8-byte)
+// take the single-touch ring scan instead (scan_ring.cuh: persistent CTAs,
+// TMA stages, tiles held in registers while they look back): 6-19% faster
+// there, slower beyond, where only the L2 covers the look-back latency.
 // The alternatives measured against this one (register-tiled single-touch,
 // TMA-staged, warp-specialized, persistent look-ahead) are summarised in
-// DESIGN.md §6 and profiles/r1_scan_limits.md.
+// DESIGN.md §6, profiles/r1_scan_limits.md and profiles/r2_scan.md.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -72,6 +76,7 @@ ga_status_t launch_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t in_dt, ga_dt
   const uintptr_t out_align = isz == osz ? 16 : 32;
   const bool aligned = ((uintptr_t)in & 15) == 0 && ((uintptr_t)out & (out_align - 1)) == 0;
   if (!aligned) return launch_shape<SHAPE_RG>(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);
+  if (use_ring(n, isz, osz)) return launch_ring(op, ex, dt, n, in, out, carry, carry_count, ws, s);
   switch (choose_shape(n, isz, osz)) {
     case SHAPE_S: return launch_shape<SHAPE_S>(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);
     case SHAPE_M: return launch_shape<SHAPE_M>(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);

@@ -1,0 +1,60 @@
+// scan_r.cu — the ring (single-touch) scan for mid-size arrays (see
+// scan_ring.cuh), every (op, kind, dtype) instance; scan.cu dispatches.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "scan_impl.cuh"
+#include "scan_ring.cuh"
+
+namespace ga {
+namespace scan_impl {
+
+namespace {
+using namespace scan_detail;
+
+template <int OP, typename T, bool EX, int W = RING_W, int R = RING_R, int S = RING_S, int F = RING_F>
+ga_status_t ring_run(int64_t n, const void *in, void *out, const void *carry, int64_t cc, void *ws, cudaStream_t s) {
+  constexpr int64_t TE = (int64_t)W * R * 512 / (int64_t)sizeof(T);
+  constexpr size_t SMEM = (size_t)S * W * R * 512;
+  auto k = scan_ring_kernel<OP, T, W, R, S, F, EX>;
+  static const cudaError_t attr = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+  if (attr != cudaSuccess) return fail(GA_ERR_CUDA, "scan (ring): %s", cudaGetErrorString(attr));
+  ScanArgs<T> p = make_args<T>(n, TE, in, out, carry, cc, ws);
+  const int64_t grid = std::min<int64_t>(sm_count(), p.num_tiles);
+  launch(k, (int)grid, ring_threads<W, F>(), SMEM, s, p);
+  count_launch();
+  return check_launch("scan_ring_kernel");
+}
+
+template <typename T>
+ga_status_t ring_by_op(ga_op_t op, bool ex, int64_t n, const void *in, void *out, const void *carry, int64_t cc,
+                       void *ws, cudaStream_t s) {
+  switch (op) {
+    case GA_OP_SUM:
+      return ex ? ring_run<GA_OP_SUM, T, true>(n, in, out, carry, cc, ws, s)
+                : ring_run<GA_OP_SUM, T, false>(n, in, out, carry, cc, ws, s);
+    case GA_OP_MAX:
+      return ex ? ring_run<GA_OP_MAX, T, true>(n, in, out, carry, cc, ws, s)
+                : ring_run<GA_OP_MAX, T, false>(n, in, out, carry, cc, ws, s);
+    case GA_OP_MIN:
+      return ex ? ring_run<GA_OP_MIN, T, true>(n, in, out, carry, cc, ws, s)
+                : ring_run<GA_OP_MIN, T, false>(n, in, out, carry, cc, ws, s);
+  }
+  return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad op %d", (int)op);
+}
+}  // namespace
+
+ga_status_t launch_ring(ga_op_t op, bool ex, ga_dtype_t dt, int64_t n, const void *in, void *out, const void *carry,
+                        int64_t cc, void *ws, cudaStream_t s) {
+  switch (dt) {
+    case GA_I32: return ring_by_op<int32_t>(op, ex, n, in, out, carry, cc, ws, s);
+    case GA_I64: return ring_by_op<int64_t>(op, ex, n, in, out, carry, cc, ws, s);
+    case GA_F32: return ring_by_op<float>(op, ex, n, in, out, carry, cc, ws, s);
+    case GA_F64: return ring_by_op<double>(op, ex, n, in, out, carry, cc, ws, s);
+    default: break;
+  }
+  return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad dtype %d", (int)dt);
+}
+
+}  // namespace scan_impl
+}  // namespace ga

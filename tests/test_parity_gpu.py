@@ -672,35 +672,39 @@ def test_ewmap_maxmin_signed_zero_bit_exact(dt):
         assert np.array_equal(bits(got[keep]), bits(ref[keep])), ew
 
 
+# 8-byte scans reach the L shape above the ring window (768 MiB of input)
+N_L8 = (768 << 20) // 8 + 12345
+
+
 @pytest.mark.parametrize("dt", [np.int64, np.float64])
 @pytest.mark.parametrize("offset", [0, 2])
 def test_scan_8byte_l_shape_both_row_widths(dt, offset):
     """8-byte scans at the L shape take 1 KiB rows (LDG/STG.256) when input and
     output are 32-byte aligned, else 512-byte rows: a view 2 elements (16
     bytes) into an allocation exercises the second path.  Integer scans are
-    exact; float64 SUM within R22."""
-    n = 256 * 24 * 32 * 64 + 12345  # >= 256 L tiles, ragged last tile
+    exact; float64 SUM over integer-valued data (prefix sums < 2^53) is exact
+    in any order and must equal the integer oracle bit for bit."""
+    n = N_L8  # ragged last tile
     if dt == np.int64:
         x = np.random.default_rng(offset + 5).integers(-(1 << 40), 1 << 40, size=n, dtype=np.int64)
     else:
-        x = host_data(dt, n, 9, signed=True)
+        k = synth.host_fill(synth.I32_RANGE, 9, n, lo=0, hi=9)
+        x = k.astype(np.float64)
     for exclusive in (False, True):
         kind = oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE
         got = G.scan(to_dev(x, offset), exclusive=exclusive).cpu().numpy()
         if dt == np.int64:
             assert np.array_equal(got, oracle.scan(kind, x))
         else:
-            ref, sa = oracle.scan(kind, x, return_sumabs=True)
-            d = np.arange(n) / 2048.0 + 512
-            assert np.all(np.abs(got - ref) <= d * 2.0 ** -53 * sa + 1e-300)
+            assert_bit_exact(got, oracle.scan(kind, k, out_dtype=np.int64).astype(np.float64))
 
 
 @pytest.mark.parametrize("offset", [0, 2])
-def test_scan_int64_l_shape_in_place(offset):
-    """In-place int64 scans at the L shape, 1 KiB rows (offset 0) and
-    512-byte rows (offset 2 elements = 16 bytes): coherent loads (the output
-    overwrites the input) on both row widths."""
-    n = 300 * 24 * 32 * 64 + 4097
+@pytest.mark.parametrize("n", [300 * 24 * 32 * 64 + 4097, N_L8])
+def test_scan_int64_l_shape_in_place(offset, n):
+    """In-place int64 scans in the ring window (118 MB) and at the L shape,
+    1 KiB rows (offset 0) and 512-byte rows (offset 2 elements = 16 bytes):
+    coherent loads (the output overwrites the input) on every path."""
     x = np.random.default_rng(77 + offset).integers(-(1 << 40), 1 << 40, size=n, dtype=np.int64)
     for exclusive in (False, True):
         d = to_dev(x, offset)
@@ -714,7 +718,7 @@ def test_scan_int64_l_shape_in_place(offset):
 def test_scan_maxmin_8byte_l_shape(dt, op):
     """MAX / MIN scans of 8-byte types at the L shape (1 KiB rows), inclusive
     and exclusive, bit-exact — float64 data zero- and NaN-heavy (R6, R7)."""
-    n = 256 * 24 * 32 * 64 + 999
+    n = N_L8 - 12345 + 999
     if dt == np.int64:
         x = np.random.default_rng(op + 3).integers(-(1 << 62), 1 << 62, size=n, dtype=np.int64)
     else:
@@ -724,3 +728,110 @@ def test_scan_maxmin_8byte_l_shape(dt, op):
         got = G.scan(to_dev(x), exclusive=exclusive, op=op).cpu().numpy()
         ref = oracle.scan(oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE, x, op=op)
         assert np.array_equal(bits(got), bits(ref))
+
+
+# ------------------------------------------------------------------ ring scan (scan_ring.cuh)
+# 16-byte aligned, non-widening scans of 48 MiB .. 384 MiB (4-byte) / 768 MiB
+# (8-byte) of input take the single-touch ring kernel: 64 KiB tiles (16384 /
+# 8192 elements), persistent CTAs, TMA stages, a ragged tail read element by
+# element past the last 16-byte multiple.
+RING_MIN = 48 << 20
+RING_MAX = {4: 384 << 20, 8: 768 << 20}
+
+
+def _ring_data(dt, op, n, seed):
+    if np.dtype(dt).kind == "f":
+        if op == oracle.SUM:  # indicator data: every prefix sum is an integer < 2^24, exact in any order
+            return (synth.host_fill(synth.I32_RANGE, seed, n, lo=0, hi=7) == 0).astype(dt)
+        x = zeros_heavy(dt, n, seed)
+        x[np.random.default_rng(seed).integers(0, n, size=256)] = np.nan
+        return x
+    info = np.iinfo(dt)
+    return np.random.default_rng(seed).integers(info.min, info.max, size=n, dtype=dt, endpoint=True)
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.int64, np.float32, np.float64])
+@pytest.mark.parametrize("op", [oracle.SUM, oracle.MAX, oracle.MIN])
+def test_scan_ring_every_op_and_dtype(dt, op):
+    """Every (op, dtype, kind) of the ring kernel against the oracle, bit for
+    bit: full-range integers (SUM wraps constantly), 0/1 floats (float SUM
+    exact in any order), zero- and NaN-heavy float MAX / MIN (R6, R7);
+    ragged last tile."""
+    n = (64 << 20) // np.dtype(dt).itemsize + 12345
+    x = _ring_data(dt, op, n, 40 + op)
+    for exclusive in (False, True):
+        kind = oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE
+        got = G.scan(to_dev(x), exclusive=exclusive, op=op).cpu().numpy()
+        if np.dtype(dt).kind == "f" and op == oracle.SUM:
+            ref = oracle.scan(kind, x.astype(np.int64)).astype(dt)
+        else:
+            ref = oracle.scan(kind, x, op=op)
+        assert_bit_exact(got, ref)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_scan_ring_float_sum_within_bound(dt):
+    """Signed random data in the ring window: R22's bound on the exact
+    prefix sums (the ring chains 64 KiB tile prefixes through the look-back;
+    inside a tile: lane-serial 16-byte chunks, warp shuffle scans, rows and
+    warps in order)."""
+    n = RING_MIN // np.dtype(dt).itemsize + 4099
+    x = host_data(dt, n, 12, signed=True)
+    u = 2.0 ** -24 if dt == np.float32 else 2.0 ** -53
+    d = np.arange(n) / 2048.0 + 512
+    for exclusive in (False, True):
+        ref, sa = oracle.scan(oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE, x, return_sumabs=True)
+        got = G.scan(to_dev(x), exclusive=exclusive).cpu().numpy().astype(np.float64)
+        assert np.all(np.abs(got - ref) <= d * u * sa + 1e-300)
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.int64])
+def test_scan_ring_window_edges(dt):
+    """Sizes either side of the ring window (M shape | ring | ring | L shape)
+    and tails of 1-3 elements past a 16-byte multiple, inclusive and
+    exclusive, wrapping data."""
+    isz = np.dtype(dt).itemsize
+    te = 65536 // isz
+    lo, hi = RING_MIN // isz, RING_MAX[isz] // isz
+    info = np.iinfo(dt)
+    for n in (lo - 1, lo, lo + 1, 1000 * te + 3, hi, hi + 1):
+        x = np.random.default_rng(n).integers(info.min, info.max, size=n, dtype=dt, endpoint=True)
+        for exclusive in (False, True):
+            kind = oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE
+            got = G.scan(to_dev(x), exclusive=exclusive).cpu().numpy()
+            assert_bit_exact(got, oracle.scan(kind, x))
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.int64, np.float32])
+def test_scan_ring_carry_inplace_and_views(dt):
+    """Ring-window sizes with a carry-in (tile 0 publishes carry (+) aggregate),
+    in place, and as a view 16 bytes into its allocation (still the ring
+    kernel) or 1 element in (the unaligned register kernel)."""
+    isz = np.dtype(dt).itemsize
+    n = (96 << 20) // isz + 5
+    if np.dtype(dt).kind == "f":
+        x = synth.host_fill(synth.I32_RANGE, 51, n, lo=-4, hi=4).astype(dt)  # |prefix| stays < 2^24: exact
+        carry = np.array([3.0, -1.0], dt)
+        c = dt(2.0)
+    else:
+        info = np.iinfo(dt)
+        x = np.random.default_rng(51).integers(info.min, info.max, size=n, dtype=dt, endpoint=True)
+        carry = np.array([info.max, 12345, -7], dt)
+        with np.errstate(over="ignore"):
+            c = dt(np.add.reduce(carry, dtype=dt))
+    def same(got, ref):  # the float oracle returns exact float64 sums (integers < 2^24 here)
+        if np.dtype(dt).kind == "f":
+            assert np.array_equal(got.astype(np.float64), ref)
+        else:
+            assert_bit_exact(got, ref)
+
+    for ex in (False, True):
+        kind = oracle.EXCLUSIVE if ex else oracle.INCLUSIVE
+        got = G.scan(to_dev(x), exclusive=ex, carry=to_dev(carry)).cpu().numpy()
+        same(got, oracle.scan(kind, x, carry=c))
+        xd = to_dev(x)
+        G.scan(xd, exclusive=ex, out=xd)
+        same(xd.cpu().numpy(), oracle.scan(kind, x))
+        for offs in (16 // isz, 1):
+            got = G.scan(to_dev(x, offs), exclusive=ex).cpu().numpy()
+            same(got, oracle.scan(kind, x))

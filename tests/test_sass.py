@@ -59,7 +59,7 @@ def test_elementwise_float_has_no_fma(sass):
 
 
 def test_vector_widths(sass):
-    seen = {"ew": False, "red": False, "scan": False, "scan1k": False}
+    seen = {"ew": False, "red": False, "scan": False, "scan1k": False, "ring": False}
     for name, body in sass.items():
         d = demangled_kind(name)
         if "ew_vec_kernel" in d:
@@ -77,6 +77,9 @@ def test_vector_widths(sass):
                 st = r"STG\.E\S*\.256" if widen else r"STG\.E\S*\.128"  # widened rows: 32 B per lane
                 assert re.search(r"LDG\.E\S*\.128", body) and re.search(st, body), d
             seen["scan"] = True
+        if "scan_ring_kernel" in d:  # TMA bulk copies in (UBLKCP), 512-byte warp rows out
+            assert "UBLKCP" in body and re.search(r"STG\.E\S*\.128", body), d
+            seen["ring"] = True
     assert all(seen.values()), seen
 
 
@@ -84,7 +87,12 @@ def test_no_local_memory_spills():
     """cuobjdump -res-usage reports register spills as STACK (LOCAL is only
     static local arrays).  Every kernel has STACK:0 except the sin/cos maps
     (ewmap ops 7, 8) and the scalar float64 exp map (op 5), whose libm slow paths (range
-    reduction) keep a small array on the stack — not a spill."""
+    reduction) keep a small array on the stack — not a spill — and the ring
+    scan (scan_ring.cuh): its 20-warp CTA caps registers at 96, and 4-56
+    bytes of its state go to the stack (mostly one loop-invariant register
+    saved once per role loop); every spill-free shape (<= 16 warps: 12-13
+    data warps) measured 3-10% slower (profiles/r2_scan.md), so the cap is
+    kept and the stack bounded here instead."""
     out = subprocess.run(["cuobjdump", "-res-usage", LIB], capture_output=True, text=True).stdout
     locs = [int(x) for x in re.findall(r"LOCAL:(\d+)", out)]
     assert locs and max(locs) == 0
@@ -99,5 +107,8 @@ def test_no_local_memory_spills():
             stack[cur] = int(m.group(1))
     assert len(stack) > 100
     libm = re.compile(r"ewmap_(vec|scalar)_kernel<(7|8), (float|double)|ewmap_scalar_kernel<5, double>")
-    bad = [demangled_kind(k) for k, v in stack.items() if v and not libm.search(demangled_kind(k))]
+    ring = [v for k, v in stack.items() if "scan_ring_kernel" in demangled_kind(k)]
+    assert len(ring) == 24 and max(ring) <= 64, ring
+    bad = [demangled_kind(k) for k, v in stack.items()
+           if v and not libm.search(demangled_kind(k)) and "scan_ring_kernel" not in demangled_kind(k)]
     assert not bad, bad[:5]

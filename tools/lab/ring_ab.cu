@@ -1,0 +1,61 @@
+// ring_ab.cu — tuning lab only: the product ring scan (csrc/scan_r.cu, built
+// here with stub host helpers) callable for any (op, kind, dtype, n), to A/B
+// it against the product dispatch and pick scan.cu's size window.
+#include <cstdarg>
+#include <cstdio>
+
+#include "../../paper_1304_5553_b200/csrc/scan_r.cu"
+
+namespace ga {
+ga_status_t fail(ga_status_t s, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vfprintf(stderr, fmt, ap);
+  va_end(ap);
+  fputc('\n', stderr);
+  return s;
+}
+ga_status_t check_launch(const char *what) {
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GA_OK : fail(GA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int d;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+  }
+  return n;
+}
+void count_launch() {}
+}  // namespace ga
+
+extern "C" int ring_ab(int op, int ex, int dt, int64_t n, const void *in, void *out, const void *carry, int64_t cc,
+                       void *ws, void *stream) {
+  return (int)ga::scan_impl::launch_ring((ga_op_t)op, ex != 0, (ga_dtype_t)dt, n, in, out, carry, cc, ws,
+                                         (cudaStream_t)stream);
+}
+
+// shape variants (int32 / int64 SUM): v = 0 the product constants, else below
+template <typename T>
+static int ring_cfg(int v, int ex, int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
+  using namespace ga::scan_impl;
+#define RC(W, R, S, F)                                                                                          \
+  return (int)(ex ? ring_run<GA_OP_SUM, T, true, W, R, S, F>(n, in, out, nullptr, 0, ws, s)                    \
+                  : ring_run<GA_OP_SUM, T, false, W, R, S, F>(n, in, out, nullptr, 0, ws, s));
+  switch (v) {
+    case 1: RC(16, 8, 3, 2)
+    case 2: RC(12, 8, 4, 2)
+    case 3: RC(12, 10, 3, 1)
+    case 4: RC(13, 8, 4, 1)
+    case 5: RC(12, 8, 4, 1)
+    case 6: RC(8, 16, 3, 1)
+  }
+#undef RC
+  return 2;
+}
+extern "C" int ring_ab_cfg(int v, int ex, int dt, int64_t n, const void *in, void *out, void *ws, void *stream) {
+  return dt == 2 ? ring_cfg<int32_t>(v, ex, n, in, out, ws, (cudaStream_t)stream)
+                 : ring_cfg<int64_t>(v, ex, n, in, out, ws, (cudaStream_t)stream);
+}
