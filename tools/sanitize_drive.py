@@ -77,12 +77,26 @@ for n in (129 * 16384 - 3, 300 * 16384 + 5):
                 alpha_num=torch.ones(1, device=dev), alpha_den=torch.ones(1, device=dev))
     torch.cuda.synchronize()
 
-# L-shape scans (>= 256 super-tiles: the look-back L2 prefetch of the tile 42
-# ids ahead is active), in place and out of place, plus a ragged tail
-# (8-byte and widened L-shape scans read 1 KiB rows when 32-byte aligned and
-# 512-byte rows otherwise: both, via a 2-element (16-byte) view offset)
-for n, dt in ((256 * 98304 + 12345, torch.int32), (256 * 49152 + 777, torch.int64),
-              (256 * 49152 + 999, torch.float64)):
+# Ring scans (48 MiB .. 384 / 768 MiB of non-widening input: persistent CTAs,
+# TMA bulk stages, mbarriers, register double buffer): every op, in place,
+# carry-in, a 16-byte view offset, ragged tails of 1-3 elements past the last
+# 16-byte multiple (element-wise tail reads)
+for n, dt in (((48 << 20) // 4 + 3, torch.int32), ((64 << 20) // 8 + 1, torch.int64),
+              ((64 << 20) // 4 + 2, torch.float32), ((96 << 20) // 8 + 5, torch.float64)):
+    for off in (0, 2):
+        x = arr(n, dt, off)
+        for op in (G.SUM, G.MAX, G.MIN):
+            G.scan(x, op=op)
+        G.scan(x, exclusive=True, carry=arr(3, dt))
+        G.scan(x, exclusive=True, out=x)
+        torch.cuda.synchronize()
+# L-shape scans (above the ring window; >= 256 super-tiles: the look-back L2
+# prefetch of the tile 42 ids ahead is active), in place and out of place,
+# plus a ragged tail (8-byte and widened L-shape scans read 1 KiB rows when
+# 32-byte aligned and 512-byte rows otherwise: both, via a 2-element
+# (16-byte) view offset)
+for n, dt in (((384 << 20) // 4 + 12345, torch.int32), ((768 << 20) // 8 + 777, torch.int64),
+              ((768 << 20) // 8 + 999, torch.float64)):
     for off in (0, 2):
         x = arr(n, dt, off)
         G.scan(x)
