@@ -12,11 +12,17 @@ namespace scan_impl {
 namespace {
 using namespace scan_detail;
 
-template <int OP, typename T, bool EX, int W = RING_W, int R = RING_R, int S = RING_S, int F = RING_F>
+// Q: bulk loads in flight per CTA; 0 = the product choice: one for 4-byte
+// types (the tile id is drawn when the previous load has landed, which
+// narrows the spread of landing times the look-back waits on: int32 2^25
+// -6%, 2^26 -2 to -5%), all S stages for 8-byte types (one in flight was
+// 1-4% slower from 2^27; tools/lab/run_ring_ab.py cfg, profiles/r2_ring.md).
+template <int OP, typename T, bool EX, int W = RING_W, int R = RING_R, int S = RING_S, int F = RING_F, int Q0 = 0>
 ga_status_t ring_run(int64_t n, const void *in, void *out, const void *carry, int64_t cc, void *ws, cudaStream_t s) {
+  constexpr int Q = Q0 > 0 ? Q0 : sizeof(T) == 4 ? 1 : S;
   constexpr int64_t TE = (int64_t)W * R * 512 / (int64_t)sizeof(T);
   constexpr size_t SMEM = (size_t)S * W * R * 512;
-  auto k = scan_ring_kernel<OP, T, W, R, S, F, EX>;
+  auto k = scan_ring_kernel<OP, T, W, R, S, F, EX, Q>;
   static const cudaError_t attr = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
   if (attr != cudaSuccess) return fail(GA_ERR_CUDA, "scan (ring): %s", cudaGetErrorString(attr));
   ScanArgs<T> p = make_args<T>(n, TE, in, out, carry, cc, ws);

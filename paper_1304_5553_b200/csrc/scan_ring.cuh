@@ -69,7 +69,9 @@ constexpr int ring_threads() {
   return (W + 2 + F) * 32;
 }
 
-template <int OP, typename T, int W, int R, int S, int F, bool EXCLUSIVE>
+// MAXQ: bulk loads in flight per CTA (<= S): the producer draws the next
+// tile only once the load MAXQ uses back has landed.
+template <int OP, typename T, int W, int R, int S, int F, bool EXCLUSIVE, int MAXQ = S>
 __global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(ScanArgs<T> p) {
   pdl_enter();
   using O = Op<OP, T>;
@@ -143,6 +145,7 @@ __global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(Scan
     for (int64_t k = 0;; ++k) {
       const int s = (int)(k % S);
       if (k >= S) mb_wait(&empty[s], (uint32_t)((k / S - 1) & 1));
+      if (MAXQ < S && k >= MAXQ) mb_wait(&full[(k - MAXQ) % S], (uint32_t)(((k - MAXQ) / S) & 1));
       uint32_t e;
       const int64_t t = k == 0 ? (int64_t)s_first : draw(e);
       tid_ring[k % TR] = t;

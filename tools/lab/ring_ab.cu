@@ -41,16 +41,16 @@ extern "C" int ring_ab(int op, int ex, int dt, int64_t n, const void *in, void *
 template <typename T>
 static int ring_cfg(int v, int ex, int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   using namespace ga::scan_impl;
-#define RC(W, R, S, F)                                                                                          \
-  return (int)(ex ? ring_run<GA_OP_SUM, T, true, W, R, S, F>(n, in, out, nullptr, 0, ws, s)                    \
-                  : ring_run<GA_OP_SUM, T, false, W, R, S, F>(n, in, out, nullptr, 0, ws, s));
+#define RC(W, R, S, F, Q)                                                                                       \
+  return (int)(ex ? ring_run<GA_OP_SUM, T, true, W, R, S, F, Q>(n, in, out, nullptr, 0, ws, s)                 \
+                  : ring_run<GA_OP_SUM, T, false, W, R, S, F, Q>(n, in, out, nullptr, 0, ws, s));
   switch (v) {
-    case 1: RC(16, 8, 3, 2)
-    case 2: RC(12, 8, 4, 2)
-    case 3: RC(12, 10, 3, 1)
-    case 4: RC(13, 8, 4, 1)
-    case 5: RC(12, 8, 4, 1)
-    case 6: RC(8, 16, 3, 1)
+    case 1: RC(16, 8, 3, 2, 3)
+    case 2: RC(16, 8, 3, 2, 2)
+    case 3: RC(16, 8, 3, 2, 1)
+    case 4: RC(16, 4, 6, 2, 2)
+    case 5: RC(16, 4, 6, 2, 3)
+    case 6: RC(16, 4, 6, 2, 4)
   }
 #undef RC
   return 2;
