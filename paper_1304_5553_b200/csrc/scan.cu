@@ -76,7 +76,7 @@ ga_status_t launch_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t in_dt, ga_dt
   const uintptr_t out_align = isz == osz ? 16 : 32;
   const bool aligned = ((uintptr_t)in & 15) == 0 && ((uintptr_t)out & (out_align - 1)) == 0;
   if (!aligned) return launch_shape<SHAPE_RG>(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);
-  if (use_ring(n, isz, osz)) return launch_ring(op, ex, dt, n, in, out, carry, carry_count, ws, s);
+  if (use_ring(n, isz, osz)) return launch_ring(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);
   switch (choose_shape(n, isz, osz)) {
     case SHAPE_S: return launch_shape<SHAPE_S>(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);
     case SHAPE_M: return launch_shape<SHAPE_M>(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);

@@ -165,18 +165,22 @@ ga_status_t launch_shape(ga_op_t op, bool ex, ga_dtype_t in_dt, ga_dtype_t dt, i
 // (64 KiB tiles), 3 stages, 2 fold warps; non-widening, 16-byte aligned.
 constexpr int RING_W = 16, RING_R = 8, RING_S = 3, RING_F = 2;
 // Size window of the ring scan (tools/lab/run_ring_ab.py, same process, back
-// to back against the two-touch shapes; profiles/r2_scan.md): input bytes
+// to back against the two-touch shapes; profiles/r2_ring.md): input bytes
 // from 48 MiB (int32 32 MiB: even; 64 MiB: -16%) to 384 MiB for 4-byte
 // types (256 MiB: -6 to -8%; 512 MiB: even to +4%) and 768 MiB for 8-byte
-// types (512 MiB: -3 to -5%; 1 GiB: even); non-widening scans only.
+// types (512 MiB: -3 to -5%; 1 GiB: even).  Widening scans (4-byte in,
+// 8-byte out) take it from 48 MiB at any size: -17% at 64 MiB, -7% at 1 GiB,
+// -5% at 4 GiB for SUM (the widened L shape's 1 KiB rows lose to single
+// touch there); MAX within +-1.4%.
 constexpr int64_t RING_MIN_BYTES = 48ll << 20, RING_MAX_BYTES4 = 384ll << 20, RING_MAX_BYTES8 = 768ll << 20;
 inline bool use_ring(int64_t n, size_t isz, size_t osz) {
-  if (isz != osz) return false;
   const int64_t b = n * (int64_t)isz;
-  return b >= RING_MIN_BYTES && b <= (isz == 8 ? RING_MAX_BYTES8 : RING_MAX_BYTES4);
+  if (b < RING_MIN_BYTES) return false;
+  if (isz != osz) return true;
+  return b <= (isz == 8 ? RING_MAX_BYTES8 : RING_MAX_BYTES4);
 }
-ga_status_t launch_ring(ga_op_t op, bool ex, ga_dtype_t dt, int64_t n, const void *in, void *out, const void *carry,
-                        int64_t cc, void *ws, cudaStream_t s);
+ga_status_t launch_ring(ga_op_t op, bool ex, ga_dtype_t in_dt, ga_dtype_t dt, int64_t n, const void *in, void *out,
+                        const void *carry, int64_t cc, void *ws, cudaStream_t s);
 
 #define GA_SCAN_INSTANTIATE(SHAPE)                                                                                 \
   template ga_status_t launch_shape<SHAPE>(ga_op_t, bool, ga_dtype_t, ga_dtype_t, int64_t, const void *, void *, \

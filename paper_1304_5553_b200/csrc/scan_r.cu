@@ -17,41 +17,47 @@ using namespace scan_detail;
 // narrows the spread of landing times the look-back waits on: int32 2^25
 // -6%, 2^26 -2 to -5%), all S stages for 8-byte types (one in flight was
 // 1-4% slower from 2^27; tools/lab/run_ring_ab.py cfg, profiles/r2_ring.md).
-template <int OP, typename T, bool EX, int W = RING_W, int R = RING_R, int S = RING_S, int F = RING_F, int Q0 = 0>
+template <int OP, typename T, typename Tin, bool EX, int W = RING_W, int R = RING_R, int S = RING_S,
+          int F = RING_F, int Q0 = 0>
 ga_status_t ring_run(int64_t n, const void *in, void *out, const void *carry, int64_t cc, void *ws, cudaStream_t s) {
   constexpr int Q = Q0 > 0 ? Q0 : sizeof(T) == 4 ? 1 : S;
-  constexpr int64_t TE = (int64_t)W * R * 512 / (int64_t)sizeof(T);
+  constexpr int64_t TE = (int64_t)W * R * 512 / (int64_t)sizeof(Tin);
   constexpr size_t SMEM = (size_t)S * W * R * 512;
-  auto k = scan_ring_kernel<OP, T, W, R, S, F, EX, Q>;
+  auto k = scan_ring_kernel<OP, T, Tin, W, R, S, F, EX, Q>;
   static const cudaError_t attr = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
   if (attr != cudaSuccess) return fail(GA_ERR_CUDA, "scan (ring): %s", cudaGetErrorString(attr));
-  ScanArgs<T> p = make_args<T>(n, TE, in, out, carry, cc, ws);
+  ScanArgs<T, Tin> p = make_args<T, Tin>(n, TE, in, out, carry, cc, ws);
   const int64_t grid = std::min<int64_t>(sm_count(), p.num_tiles);
   launch(k, (int)grid, ring_threads<W, F>(), SMEM, s, p);
   count_launch();
   return check_launch("scan_ring_kernel");
 }
 
-template <typename T>
+template <typename T, typename Tin = T>
 ga_status_t ring_by_op(ga_op_t op, bool ex, int64_t n, const void *in, void *out, const void *carry, int64_t cc,
                        void *ws, cudaStream_t s) {
   switch (op) {
     case GA_OP_SUM:
-      return ex ? ring_run<GA_OP_SUM, T, true>(n, in, out, carry, cc, ws, s)
-                : ring_run<GA_OP_SUM, T, false>(n, in, out, carry, cc, ws, s);
+      return ex ? ring_run<GA_OP_SUM, T, Tin, true>(n, in, out, carry, cc, ws, s)
+                : ring_run<GA_OP_SUM, T, Tin, false>(n, in, out, carry, cc, ws, s);
     case GA_OP_MAX:
-      return ex ? ring_run<GA_OP_MAX, T, true>(n, in, out, carry, cc, ws, s)
-                : ring_run<GA_OP_MAX, T, false>(n, in, out, carry, cc, ws, s);
+      return ex ? ring_run<GA_OP_MAX, T, Tin, true>(n, in, out, carry, cc, ws, s)
+                : ring_run<GA_OP_MAX, T, Tin, false>(n, in, out, carry, cc, ws, s);
     case GA_OP_MIN:
-      return ex ? ring_run<GA_OP_MIN, T, true>(n, in, out, carry, cc, ws, s)
-                : ring_run<GA_OP_MIN, T, false>(n, in, out, carry, cc, ws, s);
+      return ex ? ring_run<GA_OP_MIN, T, Tin, true>(n, in, out, carry, cc, ws, s)
+                : ring_run<GA_OP_MIN, T, Tin, false>(n, in, out, carry, cc, ws, s);
   }
   return fail(GA_ERR_INVALID_ARGUMENT, "scan: bad op %d", (int)op);
 }
 }  // namespace
 
-ga_status_t launch_ring(ga_op_t op, bool ex, ga_dtype_t dt, int64_t n, const void *in, void *out, const void *carry,
-                        int64_t cc, void *ws, cudaStream_t s) {
+ga_status_t launch_ring(ga_op_t op, bool ex, ga_dtype_t in_dt, ga_dtype_t dt, int64_t n, const void *in, void *out,
+                        const void *carry, int64_t cc, void *ws, cudaStream_t s) {
+  if (in_dt != dt) {
+    if (in_dt == GA_I32 && dt == GA_I64) return ring_by_op<int64_t, int32_t>(op, ex, n, in, out, carry, cc, ws, s);
+    if (in_dt == GA_F32 && dt == GA_F64) return ring_by_op<double, float>(op, ex, n, in, out, carry, cc, ws, s);
+    return fail(GA_ERR_UNSUPPORTED, "scan %d -> %d not instantiated", (int)in_dt, (int)dt);
+  }
   switch (dt) {
     case GA_I32: return ring_by_op<int32_t>(op, ex, n, in, out, carry, cc, ws, s);
     case GA_I64: return ring_by_op<int64_t>(op, ex, n, in, out, carry, cc, ws, s);

@@ -71,15 +71,19 @@ constexpr int ring_threads() {
 
 // MAXQ: bulk loads in flight per CTA (<= S): the producer draws the next
 // tile only once the load MAXQ uses back has landed.
-template <int OP, typename T, int W, int R, int S, int F, bool EXCLUSIVE, int MAXQ = S>
-__global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(ScanArgs<T> p) {
+// Tin != T: the widening scans (int32 -> int64, float -> double), the input
+// converted where it is folded; a row then stores 32 bytes per lane.
+template <int OP, typename T, typename Tin, int W, int R, int S, int F, bool EXCLUSIVE, int MAXQ = S>
+__global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(ScanArgs<T, Tin> p) {
   pdl_enter();
   using O = Op<OP, T>;
   using namespace ring;
-  constexpr int E = 16 / (int)sizeof(T);  // elements per lane per 512-byte row
+  constexpr int E = 16 / (int)sizeof(Tin);  // elements per lane per 512-byte input row
   constexpr int ROW = 32 * E;
-  constexpr int TB = W * R * 512;  // tile bytes
-  constexpr int64_t TE = TB / (int64_t)sizeof(T);
+  constexpr int TB = W * R * 512;  // tile input bytes
+  constexpr int64_t TE = TB / (int64_t)sizeof(Tin);
+  constexpr bool WIDEN = sizeof(T) != sizeof(Tin);
+  static_assert(!WIDEN || (sizeof(T) == 8 && sizeof(Tin) == 4), "widening is 4 -> 8 bytes");
   constexpr int PIECES = 4, PB = TB / PIECES;  // bulk copies per stage
   constexpr int DEPTH = sizeof(T) == 8 ? 4 : 8;
   static_assert(TR >= S + 3, "ring too short for the stages");
@@ -107,18 +111,25 @@ __global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(Scan
   // input bytes of tile t moved by the bulk copies (a multiple of 16; the
   // ragged tail beyond them is read element by element)
   auto bulk_bytes = [&](int64_t t) -> int64_t {
-    const int64_t b = (p.n - t * TE) * (int64_t)sizeof(T);
+    const int64_t b = (p.n - t * TE) * (int64_t)sizeof(Tin);
     return b >= TB ? TB : (b & ~(int64_t)15);
   };
   // 16 bytes (E elements) at byte offset `off` of tile t: from the stage, or
   // (ragged tile, past the bulk bytes) from global memory, neutral past n
   auto chunk = [&](const unsigned char *stage, int64_t t, int off, int64_t bulk) -> uint4 {
     if (off + 16 <= bulk) return *reinterpret_cast<const uint4 *>(stage + off);
-    const int64_t i = t * TE + off / (int)sizeof(T);
-    T e[E];
+    const int64_t i = t * TE + off / (int)sizeof(Tin);
+    Tin e[E];
 #pragma unroll
-    for (int k = 0; k < E; ++k) e[k] = i + k < p.n ? p.in[i + k] : neutral;
-    return Chunk<T>::pack(e);
+    for (int k = 0; k < E; ++k) e[k] = i + k < p.n ? p.in[i + k] : Op<OP, Tin>::neutral();
+    return Chunk<Tin>::pack(e);
+  };
+  // the E input elements of a raw 16-byte chunk, converted to T
+  auto unpack = [&](const uint4 &raw, T (&v)[E]) {
+    Tin e[E];
+    Chunk<Tin>::unpack(raw, e);
+#pragma unroll
+    for (int k = 0; k < E; ++k) v[k] = (T)e[k];
   };
 
   if (threadIdx.x == 0) {
@@ -193,7 +204,7 @@ __global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(Scan
 #pragma unroll 8
         for (int i = 0; i < TB / (F * 512); ++i) {
           T e[E];
-          Chunk<T>::unpack(*reinterpret_cast<const uint4 *>(stage + (i * F * 32 + f * 32 + lane) * 16), e);
+          unpack(*reinterpret_cast<const uint4 *>(stage + (i * F * 32 + f * 32 + lane) * 16), e);
 #pragma unroll
           for (int q = 0; q < E; ++q) a = O::fold(a, e[q]);
         }
@@ -201,7 +212,7 @@ __global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(Scan
 #pragma unroll 1
         for (int i = 0; i < TB / (F * 512); ++i) {
           T e[E];
-          Chunk<T>::unpack(chunk(stage, t, (i * F * 32 + f * 32 + lane) * 16, bulk), e);
+          unpack(chunk(stage, t, (i * F * 32 + f * 32 + lane) * 16, bulk), e);
 #pragma unroll
           for (int q = 0; q < E; ++q) a = O::fold(a, e[q]);
         }
@@ -219,7 +230,7 @@ __global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(Scan
         asm volatile("bar.sync 2, %0;" ::"n"(F * 32) : "memory");
       }
       if (f == 0 && lane == 0) {
-        if (t == 0) p.status.publish(0, epoch, FLAG_INCLUSIVE, O::fold(carry_in<OP, T, T>(p), a));
+        if (t == 0) p.status.publish(0, epoch, FLAG_INCLUSIVE, O::fold(carry_in<OP, T, Tin>(p), a));
         else p.status.publish(t, epoch, FLAG_AGGREGATE, a);
         agg_ring[k % TR] = a;
         mb_arrive(&folded[k % TR]);
@@ -236,7 +247,7 @@ __global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(Scan
       mb_wait(&folded[k % TR], (uint32_t)((k / TR) & 1));  // our AGGREGATE is out
       T P;
       if (t == 0) {
-        P = carry_in<OP, T, T>(p);
+        P = carry_in<OP, T, Tin>(p);
       } else {
         P = look_back<OP, T, DEPTH>(p.status, t, epoch);
         if (lane == 0) p.status.publish(t, epoch, FLAG_INCLUSIVE, O::fold(P, agg_ring[k % TR]));
@@ -273,7 +284,7 @@ __global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(Scan
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         T e[E];
-        Chunk<T>::unpack(v[r], e);
+        unpack(v[r], e);
 #pragma unroll
         for (int q = 0; q < E; ++q) a = O::fold(a, e[q]);
       }
@@ -293,7 +304,7 @@ __global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(Scan
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         T e[E], o[E];
-        Chunk<T>::unpack(v[r], e);
+        unpack(v[r], e);
 #pragma unroll
         for (int q = 1; q < E; ++q) e[q] = O::fold(e[q - 1], e[q]);
         const T x = warp_inclusive<OP, T>(e[E - 1], lane);
@@ -306,7 +317,14 @@ __global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(Scan
         }
         const int64_t i = i0 + (int64_t)r * ROW;
         if (full_tile || i + E <= p.n) {
-          l2::stg128_hint(p.out + i, Chunk<T>::pack(o), drop);
+          if constexpr (WIDEN) {  // 4 outputs of 8 bytes: one 32-byte store per lane
+            V32 w;
+#pragma unroll
+            for (int q = 0; q < E; ++q) vset<T>(w, q, o[q]);
+            l2::stg256v_hint(p.out + i, w, drop);
+          } else {
+            l2::stg128_hint(p.out + i, Chunk<T>::pack(o), drop);
+          }
         } else {
 #pragma unroll
           for (int q = 0; q < E; ++q)

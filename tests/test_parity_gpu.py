@@ -835,3 +835,35 @@ def test_scan_ring_carry_inplace_and_views(dt):
         for offs in (16 // isz, 1):
             got = G.scan(to_dev(x, offs), exclusive=ex).cpu().numpy()
             same(got, oracle.scan(kind, x))
+
+
+@pytest.mark.parametrize("op", [oracle.SUM, oracle.MAX, oracle.MIN])
+def test_scan_ring_widening(op):
+    """Widening scans of >= 48 MiB of input take the ring kernel (8-byte scan
+    type, 32-byte stores per lane): int32 -> int64 full-range data bit-exact
+    (no int32 wrap), float32 -> float64 MAX / MIN bit-exact and SUM within
+    R22 with u = 2^-53; the 32-byte-aligned output rule (a 16-byte output
+    offset goes to the register kernel); carry-in."""
+    n = RING_MIN // 4 + 4099
+    x = np.random.default_rng(60 + op).integers(-(1 << 31), (1 << 31) - 1, size=n, dtype=np.int32, endpoint=True)
+    for exclusive in (False, True):
+        kind = oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE
+        ref = oracle.scan(kind, x, op=op, out_dtype=np.int64)
+        for out_offs in (0, 2):
+            out = torch.empty(n + out_offs, dtype=torch.int64, device=DEV)[out_offs:]
+            got = G.scan(to_dev(x), exclusive=exclusive, op=op, out=out, out_dtype=torch.int64)
+            assert_bit_exact(got.cpu().numpy(), ref)
+    f = host_data(np.float32, n, 61, signed=True)
+    d = np.arange(n) / 2048.0 + 512
+    for exclusive in (False, True):
+        kind = oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE
+        got = G.scan(to_dev(f), exclusive=exclusive, op=op, out_dtype=torch.float64).cpu().numpy()
+        if op == oracle.SUM:
+            ref, sa = oracle.scan(kind, f, return_sumabs=True, out_dtype=np.float64)
+            assert np.all(np.abs(got - ref) <= d * 2.0 ** -53 * sa + 1e-300)
+        else:
+            assert_bit_exact(got, oracle.scan(kind, f, op=op, out_dtype=np.float64))
+    if op == oracle.SUM:
+        carry = np.array([-(1 << 40), 7], np.int64)
+        got = G.scan(to_dev(x), exclusive=True, carry=to_dev(carry), out_dtype=torch.int64).cpu().numpy()
+        assert_bit_exact(got, oracle.scan(oracle.EXCLUSIVE, x, carry=np.int64(-(1 << 40) + 7), out_dtype=np.int64))

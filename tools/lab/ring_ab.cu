@@ -33,8 +33,10 @@ void count_launch() {}
 
 extern "C" int ring_ab(int op, int ex, int dt, int64_t n, const void *in, void *out, const void *carry, int64_t cc,
                        void *ws, void *stream) {
-  return (int)ga::scan_impl::launch_ring((ga_op_t)op, ex != 0, (ga_dtype_t)dt, n, in, out, carry, cc, ws,
-                                         (cudaStream_t)stream);
+  // dt < 0: the widening scan from dtype -dt - 1 (int32 -> int64, float32 -> float64)
+  const ga_dtype_t o = (ga_dtype_t)(dt < 0 ? (-dt - 1 == GA_I32 ? GA_I64 : GA_F64) : dt);
+  const ga_dtype_t i = (ga_dtype_t)(dt < 0 ? -dt - 1 : dt);
+  return (int)ga::scan_impl::launch_ring((ga_op_t)op, ex != 0, i, o, n, in, out, carry, cc, ws, (cudaStream_t)stream);
 }
 
 // shape variants (int32 / int64 SUM): v = 0 the product constants, else below
@@ -42,8 +44,8 @@ template <typename T>
 static int ring_cfg(int v, int ex, int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   using namespace ga::scan_impl;
 #define RC(W, R, S, F, Q)                                                                                       \
-  return (int)(ex ? ring_run<GA_OP_SUM, T, true, W, R, S, F, Q>(n, in, out, nullptr, 0, ws, s)                 \
-                  : ring_run<GA_OP_SUM, T, false, W, R, S, F, Q>(n, in, out, nullptr, 0, ws, s));
+  return (int)(ex ? ring_run<GA_OP_SUM, T, T, true, W, R, S, F, Q>(n, in, out, nullptr, 0, ws, s)              \
+                  : ring_run<GA_OP_SUM, T, T, false, W, R, S, F, Q>(n, in, out, nullptr, 0, ws, s));
   switch (v) {
     case 1: RC(16, 8, 3, 2, 3)
     case 2: RC(16, 8, 3, 2, 2)

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 LIB = os.path.join(HERE, "libring_ab.so")
-DT = {"int32": 2, "int64": 3, "float32": 0, "float64": 1}
+DT = {"int32": 2, "int64": 3, "float32": 0, "float64": 1, "int32w": -3, "float32w": -1}  # w: widening
 
 
 def build():
@@ -35,34 +35,36 @@ def main():
     s = torch.cuda.current_stream().cuda_stream
     ws = torch.zeros(256 + 16 * ((1 << hi) // 1024 + 64), dtype=torch.uint8, device=dev)
     for name in dts:
-        dt = getattr(torch, name)
+        dt = getattr(torch, name.rstrip("w"))
+        wide = {"int32w": torch.int64, "float32w": torch.float64}.get(name)
         N = 1 << hi
         if dt.is_floating_point:
             x = torch.rand(N, dtype=dt, device=dev)
         else:
             x = torch.randint(0, 10, (N,), dtype=dt, device=dev)
-        o = torch.empty_like(x)
+        o = torch.empty(N, dtype=wide or dt, device=dev)
         for lg in range(lo, hi + 1):
             n = (1 << lg) + (lg % 3) * 17  # some sizes ragged
             if n > N:
                 n = 1 << lg
             reps = max(3, min(50, (1 << 28) // n))
             line = []
-            for op, ex in ((0, 1), (0, 0)) + (((1, 0),) if name == "int32" else ()):
+            for op, ex in ((0, 1), (0, 0)) + (((1, 0),) if name in ("int32", "int32w") else ()):
                 opn = ["sum", "max", "min"][op]
                 gop = op
-                ref = G.scan(x[:n], exclusive=bool(ex), op=gop)
+                ref = G.scan(x[:n], exclusive=bool(ex), op=gop, out_dtype=wide)
                 for arm in ("prod", "ring"):
                     src, out = x[:n], o[:n]
 
                     def call():
                         if arm == "prod":
-                            G.scan(src, exclusive=bool(ex), op=gop, out=out)
+                            G.scan(src, exclusive=bool(ex), op=gop, out=out, out_dtype=wide)
                         else:
                             rc = L.ring_ab(op, ex, DT[name], n, src.data_ptr(), out.data_ptr(), None, 0,
                                            ws.data_ptr(), s)
                             assert rc == 0, rc
                     out.fill_(7)
+                    ok = True
                     call()
                     torch.cuda.synchronize()
                     if dt.is_floating_point and op == 0:
