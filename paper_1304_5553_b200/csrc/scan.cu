@@ -29,10 +29,12 @@
 // id resets the counter.
 // Tile 0's exclusive prefix is the carry-in c = sum(carry[0..carry_count)),
 // which is how a sharded scan injects the totals of earlier shards.
-// Mid-size arrays (48 MiB .. 384 MiB of 4-byte input, .. 768 MiB of 8-byte)
-// take the single-touch ring scan instead (scan_ring.cuh: persistent CTAs,
-// TMA stages, tiles held in registers while they look back): 6-19% faster
-// there, slower beyond, where only the L2 covers the look-back latency.
+// From 48 MiB of input up to 4 GiB (4-byte types), 768 MiB (8-byte) or
+// without bound (widening) the single-touch ring scan runs instead
+// (scan_ring.cuh: persistent CTAs, TMA stages, tiles held in registers while
+// they look back, 4-byte tiles prefetched into L2 one draw ahead): 3-19%
+// faster there; beyond, only the two-touch kernel's L2 buffer covers the
+// look-back latency.
 // The alternatives measured against this one (register-tiled single-touch,
 // TMA-staged, warp-specialized, persistent look-ahead) are summarised in
 // DESIGN.md §6, profiles/r1_scan_limits.md and profiles/r2_scan.md.

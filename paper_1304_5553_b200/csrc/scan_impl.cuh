@@ -165,14 +165,17 @@ ga_status_t launch_shape(ga_op_t op, bool ex, ga_dtype_t in_dt, ga_dtype_t dt, i
 // (64 KiB tiles), 3 stages, 2 fold warps; non-widening, 16-byte aligned.
 constexpr int RING_W = 16, RING_R = 8, RING_S = 3, RING_F = 2;
 // Size window of the ring scan (tools/lab/run_ring_ab.py, same process, back
-// to back against the two-touch shapes; profiles/r2_ring.md): input bytes
-// from 48 MiB (int32 32 MiB: even; 64 MiB: -16%) to 384 MiB for 4-byte
-// types (256 MiB: -6 to -8%; 512 MiB: even to +4%) and 768 MiB for 8-byte
-// types (512 MiB: -3 to -5%; 1 GiB: even).  Widening scans (4-byte in,
-// 8-byte out) take it from 48 MiB at any size: -17% at 64 MiB, -7% at 1 GiB,
-// -5% at 4 GiB for SUM (the widened L shape's 1 KiB rows lose to single
-// touch there); MAX within +-1.4%.
-constexpr int64_t RING_MIN_BYTES = 48ll << 20, RING_MAX_BYTES4 = 384ll << 20, RING_MAX_BYTES8 = 768ll << 20;
+// to back against the two-touch shapes; profiles/r2_ring.md): from 48 MiB of
+// input (int32 32 MiB: even; 64 MiB: -16%) up to
+//   4 GiB for 4-byte types (with the one-tile L2 prefetch: 2^28 -8%, 2^30
+//        -1 to -3%; 2^31: even to +6%, 2^32-2^33: even to +4%),
+//   768 MiB for 8-byte types (512 MiB: -3 to -5%; 1 GiB: even; beyond it
+//        +2 to +15%),
+//   any size for widening scans (4-byte in, 8-byte out: -17% at 64 MiB, -7%
+//        at 1 GiB, -5% at 4 GiB for SUM; the input arrives at a third of the
+//        traffic rate, so the on-chip buffer covers the look-back; MAX within
+//        +-1.4%).
+constexpr int64_t RING_MIN_BYTES = 48ll << 20, RING_MAX_BYTES4 = 4ll << 30, RING_MAX_BYTES8 = 768ll << 20;
 inline bool use_ring(int64_t n, size_t isz, size_t osz) {
   const int64_t b = n * (int64_t)isz;
   if (b < RING_MIN_BYTES) return false;

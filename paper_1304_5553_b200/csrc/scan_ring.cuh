@@ -73,7 +73,9 @@ constexpr int ring_threads() {
 // tile only once the load MAXQ uses back has landed.
 // Tin != T: the widening scans (int32 -> int64, float -> double), the input
 // converted where it is folded; a row then stores 32 bytes per lane.
-template <int OP, typename T, typename Tin, int W, int R, int S, int F, bool EXCLUSIVE, int MAXQ = S>
+// PFN: tile ids drawn this many uses ahead, their input prefetched into L2
+// (cp.async.bulk.prefetch.L2) so that the stage's bulk copy later hits L2.
+template <int OP, typename T, typename Tin, int W, int R, int S, int F, bool EXCLUSIVE, int MAXQ = S, int PFN = 0>
 __global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(ScanArgs<T, Tin> p) {
   pdl_enter();
   using O = Op<OP, T>;
@@ -153,12 +155,48 @@ __global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(Scan
   if (warp == W) {  // ---------------------------------------------------------- producer
     if (lane != 0) return;
     const uint64_t drop = l2::policy_evict_first();
+    const uint64_t keep = l2::policy_evict_last();
+    // FIFO of ids drawn ahead (PFN > 0): the id handed out next plus up to
+    // PFN more, each prefetched into L2 when drawn; drawing stops after the
+    // CTA's one id past the last tile.  Fixed-index register array.
+    int64_t ahead[PFN + 1];
+    int nahead = 0;
+    bool more = true;
+    auto next_id = [&](bool first) -> int64_t {
+      uint32_t e;
+      if constexpr (PFN == 0) {
+        return first ? (int64_t)s_first : draw(e);
+      } else {
+        if (first) {
+          ahead[0] = (int64_t)s_first;
+          nahead = 1;
+          more = (int64_t)s_first < nt;
+        }
+        while (more && nahead < PFN + 1) {
+          const int64_t d = draw(e);
+          more = d < nt;
+          if (more && bulk_bytes(d) > 0)
+            asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(
+                             reinterpret_cast<const unsigned char *>(p.in) + d * (int64_t)TB),
+                         "r"((uint32_t)bulk_bytes(d)), "l"(keep)
+                         : "memory");
+#pragma unroll
+          for (int i = 0; i <= PFN; ++i)
+            if (i == nahead) ahead[i] = d;
+          ++nahead;
+        }
+        const int64_t t = ahead[0];
+#pragma unroll
+        for (int i = 0; i < PFN; ++i) ahead[i] = ahead[i + 1];
+        --nahead;
+        return t;
+      }
+    };
     for (int64_t k = 0;; ++k) {
       const int s = (int)(k % S);
       if (k >= S) mb_wait(&empty[s], (uint32_t)((k / S - 1) & 1));
       if (MAXQ < S && k >= MAXQ) mb_wait(&full[(k - MAXQ) % S], (uint32_t)(((k - MAXQ) / S) & 1));
-      uint32_t e;
-      const int64_t t = k == 0 ? (int64_t)s_first : draw(e);
+      const int64_t t = next_id(k == 0);
       tid_ring[k % TR] = t;
       __threadfence_block();
       *reinterpret_cast<volatile int64_t *>(&issued) = k + 1;

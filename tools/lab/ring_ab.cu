@@ -40,24 +40,29 @@ extern "C" int ring_ab(int op, int ex, int dt, int64_t n, const void *in, void *
 }
 
 // shape variants (int32 / int64 SUM): v = 0 the product constants, else below
-template <typename T>
+template <typename T, typename Tin = T>
 static int ring_cfg(int v, int ex, int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   using namespace ga::scan_impl;
-#define RC(W, R, S, F, Q)                                                                                       \
-  return (int)(ex ? ring_run<GA_OP_SUM, T, T, true, W, R, S, F, Q>(n, in, out, nullptr, 0, ws, s)              \
-                  : ring_run<GA_OP_SUM, T, T, false, W, R, S, F, Q>(n, in, out, nullptr, 0, ws, s));
+#define RC(W, R, S, F, Q, PF)                                                                                   \
+  return (int)(ex ? ring_run<GA_OP_SUM, T, Tin, true, W, R, S, F, Q, PF>(n, in, out, nullptr, 0, ws, s)        \
+                  : ring_run<GA_OP_SUM, T, Tin, false, W, R, S, F, Q, PF>(n, in, out, nullptr, 0, ws, s));
   switch (v) {
-    case 1: RC(16, 8, 3, 2, 3)
-    case 2: RC(16, 8, 3, 2, 2)
-    case 3: RC(16, 8, 3, 2, 1)
-    case 4: RC(16, 4, 6, 2, 2)
-    case 5: RC(16, 4, 6, 2, 3)
-    case 6: RC(16, 4, 6, 2, 4)
+    case 1: RC(16, 8, 3, 2, 0, 0)
+    case 2: RC(16, 8, 3, 2, 0, 1)
+    case 3: RC(16, 8, 3, 2, 1, 1)
+    case 4: RC(16, 8, 3, 2, 1, 2)
+    case 5: RC(16, 8, 3, 2, 2, 1)
+    case 6: RC(16, 8, 3, 2, 1, 0)
+    case 7: RC(16, 8, 3, 2, 2, 2)
+    case 8: RC(16, 8, 3, 2, 3, 0)
+    case 9: RC(16, 8, 3, 2, 3, 1)
   }
 #undef RC
   return 2;
 }
 extern "C" int ring_ab_cfg(int v, int ex, int dt, int64_t n, const void *in, void *out, void *ws, void *stream) {
+  if (dt == 0) return ring_cfg<float>(v, ex, n, in, out, ws, (cudaStream_t)stream);
+  if (dt == -3) return ring_cfg<int64_t, int32_t>(v, ex, n, in, out, ws, (cudaStream_t)stream);
   return dt == 2 ? ring_cfg<int32_t>(v, ex, n, in, out, ws, (cudaStream_t)stream)
                  : ring_cfg<int64_t>(v, ex, n, in, out, ws, (cudaStream_t)stream);
 }

@@ -95,28 +95,31 @@ def cfg():
     lo, hi = int(sys.argv[2]), int(sys.argv[3])
     vs = [int(v) for v in sys.argv[4].split(",")]
     L = ctypes.CDLL(LIB)
+    DT["float32"] = 0
     L.ring_ab_cfg.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p,
                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     dev = torch.device("cuda:0")
     s = torch.cuda.current_stream().cuda_stream
     ws = torch.zeros(256 + 16 * ((1 << hi) // 1024 + 64), dtype=torch.uint8, device=dev)
-    for name in ("int32", "int64"):
-        dt = getattr(torch, name)
-        x = torch.randint(-(1 << 20), 1 << 20, (1 << hi,), dtype=dt, device=dev)
-        o = torch.empty_like(x)
+    for name in (sys.argv[5].split(",") if len(sys.argv) > 5 else ("int32", "int64")):
+        dt = getattr(torch, name.rstrip("w"))
+        wide = torch.int64 if name == "int32w" else None
+        x = torch.randint(-(1 << 20), 1 << 20, (1 << hi,), dtype=dt, device=dev) if not dt.is_floating_point \
+            else torch.randint(0, 2, (1 << hi,), dtype=torch.int32, device=dev).to(dt)
+        o = torch.empty(1 << hi, dtype=wide or dt, device=dev)
         for lg in range(lo, hi + 1):
             n = (1 << lg) + 5
             n = min(n, 1 << hi)
             reps = max(3, min(50, (1 << 28) // n))
             for ex in (1, 0):
-                ref = G.scan(x[:n], exclusive=bool(ex))
+                ref = G.scan(x[:n], exclusive=bool(ex), out_dtype=wide)
                 line = []
                 for v in [-1] + vs:
                     src, out = x[:n], o[:n]
 
                     def call():
                         if v < 0:
-                            G.scan(src, exclusive=bool(ex), out=out)
+                            G.scan(src, exclusive=bool(ex), out=out, out_dtype=wide)
                         else:
                             assert L.ring_ab_cfg(v, ex, DT[name], n, src.data_ptr(), out.data_ptr(), ws.data_ptr(),
                                                  s) == 0
