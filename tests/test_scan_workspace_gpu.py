@@ -25,6 +25,7 @@ import synth  # noqa: E402
 
 if torch.cuda.is_available():
     from paper_1304_5553_b200 import _abi
+    from paper_1304_5553_b200 import gpuarray as G
 
 DEV = "cuda:0"
 # S / M / L super-tile shapes for 4-byte and 8-byte scans (scan_impl.cuh
@@ -114,3 +115,44 @@ def test_sizes_and_alignments_alternate_on_one_workspace():
                                (oracle.SUM, True, k, np.int64)):
             got = _run(ws, op, ex, x, odt, offs)
             _check(got, _ref(op, ex, x, odt), f"plan {i} op {op} {x.dtype}->{np.dtype(odt)} offs {offs}")
+
+
+def test_ring_scans_on_concurrent_streams():
+    """Ring-kernel scans (persistent CTAs holding every SM's shared memory)
+    on three streams at once, interleaved with a multi-group reduction on a
+    fourth, five rounds without a host sync: each grid draws tiles only while
+    its CTAs are resident and no tile waits on another grid, so the scans
+    must complete and match the oracle bit for bit (the binding keeps one
+    workspace per stream and element size)."""
+    n32, n64 = (96 << 20) // 4 + 13, (96 << 20) // 8 + 7
+    k = synth.host_fill(synth.I32_RANGE, 70, n32, lo=-(1 << 20), hi=1 << 20)
+    l = np.random.default_rng(71).integers(-(1 << 40), 1 << 40, size=n64, dtype=np.int64)
+    kd, ld = _dev(k), _dev(l)
+    r = synth.device_fill(synth.I32_RANGE, 72, 1 << 26, lo=-100, hi=100, device=DEV)
+    rounds = 5
+    outs = [[torch.empty(n32, dtype=torch.int32, device=DEV) for _ in range(rounds)],
+            [torch.empty(n64, dtype=torch.int64, device=DEV) for _ in range(rounds)],
+            [torch.empty(n32, dtype=torch.int64, device=DEV) for _ in range(rounds)]]
+    sums = torch.empty(rounds, dtype=torch.int32, device=DEV)
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    torch.cuda.synchronize()
+    for i in range(rounds):
+        with torch.cuda.stream(streams[0]):
+            G.scan(kd, exclusive=bool(i & 1), out=outs[0][i])
+        with torch.cuda.stream(streams[1]):
+            G.scan(ld, out=outs[1][i])
+        with torch.cuda.stream(streams[2]):
+            G.scan(kd, out=outs[2][i], out_dtype=torch.int64)
+        with torch.cuda.stream(streams[3]):
+            G.reduce(G.SUM, G.ID, r, out=sums[i:i + 1])
+    torch.cuda.synchronize()
+    ref_k = {ex: oracle.scan(oracle.EXCLUSIVE if ex else oracle.INCLUSIVE, k) for ex in (False, True)}
+    ref_l = oracle.scan(oracle.INCLUSIVE, l)
+    ref_w = oracle.scan(oracle.INCLUSIVE, k, out_dtype=np.int64)
+    rh = synth.host_fill(synth.I32_RANGE, 72, 1 << 26, lo=-100, hi=100)
+    ref_s = oracle.reduce(oracle.SUM, oracle.MAP_ID, rh)
+    for i in range(rounds):
+        _check(outs[0][i], ref_k[bool(i & 1)], f"round {i} int32")
+        _check(outs[1][i], ref_l, f"round {i} int64")
+        _check(outs[2][i], ref_w, f"round {i} int32->int64")
+        assert int(sums[i].item()) == ref_s
