@@ -871,3 +871,45 @@ def test_scan_ring_widening(op):
         carry = np.array([-(1 << 40), 7], np.int64)
         got = G.scan(to_dev(x), exclusive=True, carry=to_dev(carry), out_dtype=torch.int64).cpu().numpy()
         assert_bit_exact(got, oracle.scan(oracle.EXCLUSIVE, x, carry=np.int64(-(1 << 40) + 7), out_dtype=np.int64))
+
+
+@pytest.mark.parametrize("dt,out_dt", [(np.int32, np.int32), (np.int64, np.int64), (np.int32, np.int64),
+                                       (np.float32, np.float32)])
+def test_scan_guard_bands_every_path(dt, out_dt):
+    """Out-of-bounds write check (compute-sanitizer being unavailable on the
+    GPU pool): the output of every scan path (S, M, ring, L shape, register
+    kernel) sits between 4 KiB guard bands filled with a sentinel, at ragged
+    sizes and 16-byte-aligned and unaligned views, in place and out of place;
+    the bands must come back untouched and the results must match the
+    oracle (float: integer-valued data, exact)."""
+    isz, osz = np.dtype(dt).itemsize, np.dtype(out_dt).itemsize
+    pad = 4096 // osz
+    sizes = [4097, 3_000_017, (64 << 20) // isz + 3]           # S / M / ring
+    if isz == 8 and osz == 8:
+        sizes.append((768 << 20) // 8 + 5)                      # L shape (8-byte)
+    for n in sizes:
+        if np.dtype(dt).kind == "f":
+            x = synth.host_fill(synth.I32_RANGE, n % 97, n, lo=0, hi=1).astype(dt)
+        else:
+            x = synth.host_fill(synth.I32_RANGE if dt == np.int32 else synth.I64_RANGE, n % 97, n,
+                                lo=-(1 << 20), hi=1 << 20)
+        ref = oracle.scan(oracle.EXCLUSIVE, x, out_dtype=None if dt == out_dt else out_dt)
+        if np.dtype(dt).kind == "f":
+            ref = oracle.scan(oracle.EXCLUSIVE, x.astype(np.int64)).astype(out_dt)
+        for offs in (0, 16 // osz, 1):
+            buf = torch.full((n + 2 * pad + offs,), 0x5A5A5A5A, dtype=NPT[out_dt], device=DEV)
+            out = buf[pad + offs:pad + offs + n]
+            G.scan(to_dev(x, offs), exclusive=True, out=out, out_dtype=NPT[out_dt])
+            b = buf.cpu().numpy()
+            assert np.all(b[:pad + offs] == np.array(0x5A5A5A5A).astype(out_dt)), (n, offs, "head band")
+            assert np.all(b[pad + offs + n:] == np.array(0x5A5A5A5A).astype(out_dt)), (n, offs, "tail band")
+            assert_bit_exact(b[pad + offs:pad + offs + n], ref)
+        if dt == out_dt:  # in place, inside guard bands
+            buf = torch.full((n + 2 * pad,), 0x5A5A5A5A, dtype=NPT[dt], device=DEV)
+            v = buf[pad:pad + n]
+            v.copy_(torch.from_numpy(x))
+            G.scan(v, exclusive=True, out=v)
+            b = buf.cpu().numpy()
+            assert np.all(b[:pad] == np.array(0x5A5A5A5A).astype(dt)) and \
+                np.all(b[pad + n:] == np.array(0x5A5A5A5A).astype(dt)), (n, "in-place bands")
+            assert_bit_exact(b[pad:pad + n], ref)
