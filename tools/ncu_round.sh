@@ -13,10 +13,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/${TAG}_launches_bench.log 2>&1
 for L in 33 32 31 30; do
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-      -k regex:'ew_vec_kernel|reduce_kernel|scan_l2_kernel' -c 5 --csv --log-file gpurun_out/${TAG}_traffic_$L.csv \
+      -k regex:'ew_vec_kernel|reduce_kernel|scan_l2_kernel|scan_ring_kernel' -c 5 --csv --log-file gpurun_out/${TAG}_traffic_$L.csv \
       python bench.py --log2n-global $L --steps 3 --warmup 3 --no-cpu-baseline --no-extras \
       > gpurun_out/${TAG}_traffic_$L.log 2>&1
 done
-ncu --set full --clock-control none --import-source on -k regex:'ew_vec_kernel|reduce_kernel|scan_l2_kernel' -c 5 \
+ncu --set full --clock-control none --import-source on -k regex:'ew_vec_kernel|reduce_kernel|scan_l2_kernel|scan_ring_kernel' -c 5 \
     -o gpurun_out/${TAG}_full -f python tools/profile_ops.py 28 > gpurun_out/${TAG}_full.log 2>&1
 echo done
