@@ -21,6 +21,10 @@ void count_launch();
 // kernel by the caller through a function-local static).
 int resident_grid(const void *kernel, int block, size_t dyn_smem = 0);
 
+// Opt `kernel` into `bytes` of dynamic shared memory on the current device
+// (cached per kernel and device).
+cudaError_t allow_dyn_smem(const void *kernel, size_t bytes);
+
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Launch `kernel` on stream s with programmatic stream serialization (PDL):

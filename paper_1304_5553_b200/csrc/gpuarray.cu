@@ -62,6 +62,24 @@ int resident_grid(const void *kernel, int block, size_t dyn_smem) {
   return grid;
 }
 
+// Opt a kernel into `bytes` of dynamic shared memory on the current device,
+// once per (kernel, device): function attributes belong to a device's
+// context, so a process that drives several GPUs sets them on each.
+cudaError_t allow_dyn_smem(const void *kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, cudaError_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_pair(kernel, dev);
+  auto it = done.find(key);
+  if (it != done.end()) return it->second;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) cudaGetLastError();
+  done[key] = e;
+  return e;
+}
+
 }  // namespace ga
 
 using namespace ga;

@@ -29,7 +29,7 @@ ga_status_t ring_run(int64_t n, const void *in, void *out, const void *carry, in
   constexpr int64_t TE = (int64_t)W * R * 512 / (int64_t)sizeof(Tin);
   constexpr size_t SMEM = (size_t)S * W * R * 512;
   auto k = scan_ring_kernel<OP, T, Tin, W, R, S, F, EX, Q, PFN>;
-  static const cudaError_t attr = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+  const cudaError_t attr = allow_dyn_smem((const void *)k, SMEM);
   if (attr != cudaSuccess) return fail(GA_ERR_CUDA, "scan (ring): %s", cudaGetErrorString(attr));
   ScanArgs<T, Tin> p = make_args<T, Tin>(n, TE, in, out, carry, cc, ws);
   const int64_t grid = std::min<int64_t>(sm_count(), p.num_tiles);

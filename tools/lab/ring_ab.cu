@@ -29,6 +29,9 @@ int sm_count() {
   return n;
 }
 void count_launch() {}
+cudaError_t allow_dyn_smem(const void *kernel, size_t bytes) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
 }  // namespace ga
 
 extern "C" int ring_ab(int op, int ex, int dt, int64_t n, const void *in, void *out, const void *carry, int64_t cc,
@@ -56,6 +59,8 @@ static int ring_cfg(int v, int ex, int64_t n, const void *in, void *out, void *w
     case 7: RC(16, 8, 3, 2, 2, 2)
     case 8: RC(16, 8, 3, 2, 3, 0)
     case 9: RC(16, 8, 3, 2, 3, 1)
+    case 10: RC(16, 8, 3, 2, 3, 3)
+    case 11: RC(16, 8, 3, 2, 2, 3)
   }
 #undef RC
   return 2;
