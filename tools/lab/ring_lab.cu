@@ -69,7 +69,7 @@ __device__ __forceinline__ void mb_init(uint64_t *b, int count) {
 // earlier look-backs).  Per-use values live in rings of TR slots (tile id,
 // aggregate, prefix + their mbarriers), so a role that runs ahead of another
 // never overwrites what the slower one still needs.
-template <int W, int R, int S, int F, int NLB, int C, bool EX, int PIECES, int LBM>
+template <int W, int R, int S, int F, int NLB, int C, bool EX, int PIECES, int LBM, bool DB>
 __global__ void __launch_bounds__((W + 1 + NLB + F) * 32, C)
     ring_scan(const int32_t *__restrict__ in, int32_t *__restrict__ out, int64_t ntiles, uint64_t *status,
               unsigned long long *ticket, uint32_t epoch, uint64_t *trace) {
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__((W + 1 + NLB + F) * 32, C)
   __shared__ int64_t tid_ring[TR];
   __shared__ int64_t issued;
   __shared__ int32_t agg_ring[TR], pre_ring[TR];
-  __shared__ int32_t wt[2][W];
+  __shared__ int32_t wt[3][W];
   __shared__ int32_t ft[F];
   __shared__ int32_t incl_sm[LBM == 2 ? 512 : 1];
   constexpr bool EARLY = LBM == 1;
@@ -327,12 +327,14 @@ __global__ void __launch_bounds__((W + 1 + NLB + F) * 32, C)
   }
 
   if (w < W) {  // ------------------------------------------------------------ data
-    for (int64_t k = 0;; ++k) {
+    // load(k): wait for use k's stage, copy it into registers, release the
+    // stage, fold the warp's rows and publish the warp total; false at the
+    // sentinel.  scan(k): wait for use k's prefix, scan the rows, store.
+    auto load = [&](int64_t k, uint4 (&v)[R], int64_t &t) -> bool {
       const int s = (int)(k % S);
       mb_wait(&full[s], (uint32_t)((k / S) & 1));
-      const int64_t t = *reinterpret_cast<volatile int64_t *>(&tid_ring[k % TR]);
-      if (t >= ntiles) return;
-      uint4 v[R];
+      t = *reinterpret_cast<volatile int64_t *>(&tid_ring[k % TR]);
+      if (t >= ntiles) return false;
       const char *st = smem + s * TB + (w * R) * 512 + lane * 16;
 #pragma unroll
       for (int r = 0; r < R; ++r) v[r] = *reinterpret_cast<const uint4 *>(st + r * 512);
@@ -344,10 +346,13 @@ __global__ void __launch_bounds__((W + 1 + NLB + F) * 32, C)
       for (int r = 0; r < R; ++r) a += (int32_t)v[r].x + (int32_t)v[r].y + (int32_t)v[r].z + (int32_t)v[r].w;
 #pragma unroll
       for (int d = 16; d; d >>= 1) a += __shfl_xor_sync(0xffffffffu, a, d);
-      if (lane == 0) wt[k & 1][w] = a;
+      if (lane == 0) wt[k % 3][w] = a;
       asm volatile("bar.sync 3, %0;" ::"n"(W * 32) : "memory");
+      return true;
+    };
+    auto scan = [&](int64_t k, const uint4 (&v)[R], int64_t t) {
       int32_t carry = 0;
-      for (int i = 0; i < w; ++i) carry += wt[k & 1][i];
+      for (int i = 0; i < w; ++i) carry += wt[k % 3][i];
       mb_wait(&pref[k % TR], (uint32_t)((k / TR) & 1));
       carry += *reinterpret_cast<volatile int32_t *>(&pre_ring[k % TR]);
       if (w == 0 && lane == 0) TRC(6)
@@ -381,6 +386,25 @@ __global__ void __launch_bounds__((W + 1 + NLB + F) * 32, C)
                      : "memory");
       }
       if (w == 0 && lane == 0) TRC(7)
+    };
+    uint4 va[R], vb[R];
+    int64_t ta, tb;
+    if (!DB) {
+      for (int64_t k = 0;; ++k) {
+        if (!load(k, va, ta)) return;
+        scan(k, va, ta);
+      }
+    }
+    // two tiles in registers: tile k waits for its prefix while k+1 is
+    // already copied out of its stage
+    if (!load(0, va, ta)) return;
+    for (int64_t k = 0;; k += 2) {
+      const bool hb = load(k + 1, vb, tb);
+      scan(k, va, ta);
+      if (!hb) return;
+      const bool ha = load(k + 2, va, ta);
+      scan(k + 1, vb, tb);
+      if (!ha) return;
     }
   }
 }
@@ -395,15 +419,15 @@ int sms() {
   return n;
 }
 
-template <int W, int R, int S, int F, int NLB, int C, int PIECES, int EARLY>
+template <int W, int R, int S, int F, int NLB, int C, int PIECES, int EARLY, bool DB>
 int run(int ex, int64_t n, const int32_t *in, int32_t *out, uint64_t *status, unsigned long long *ticket,
         uint32_t epoch, cudaStream_t st, uint64_t *trace = nullptr) {
   constexpr int TB = W * R * 512;
   constexpr int TE = TB / 4;
   if (n % TE) return 3;
   const int64_t ntiles = n / TE;
-  auto k0 = ring_scan<W, R, S, F, NLB, C, false, PIECES, EARLY>;
-  auto k1 = ring_scan<W, R, S, F, NLB, C, true, PIECES, EARLY>;
+  auto k0 = ring_scan<W, R, S, F, NLB, C, false, PIECES, EARLY, DB>;
+  auto k1 = ring_scan<W, R, S, F, NLB, C, true, PIECES, EARLY, DB>;
   static bool init = false;
   if (!init) {
     cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, S * TB);
@@ -423,16 +447,16 @@ int run(int ex, int64_t n, const int32_t *in, int32_t *out, uint64_t *status, un
 // id: W data warps, R rows per warp (512 B), S stages, F fold warps, NLB look-back warps, C CTAs per SM,
 // bulk pieces, look-back from issue (EARLY) or from landing
 #define V(X)                                 \
-  X(0, 16, 8, 3, 2, 1, 1, 4, 0)              \
-  X(1, 16, 8, 3, 2, 1, 1, 4, 2)              \
-  X(2, 16, 8, 3, 4, 1, 1, 4, 2)              \
-  X(3, 16, 4, 6, 4, 1, 1, 2, 2)              \
-  X(4, 8, 16, 3, 4, 1, 1, 4, 2)              \
-  X(5, 16, 4, 3, 2, 1, 2, 2, 2)              \
-  X(6, 16, 8, 2, 4, 1, 1, 4, 2)              \
-  X(7, 8, 8, 3, 2, 1, 2, 2, 2)               \
-  X(8, 16, 4, 4, 4, 1, 1, 2, 2)              \
-  X(9, 16, 4, 5, 4, 1, 1, 2, 2)
+  X(0, 16, 8, 1, 2, 1, 1, 4, 0, true)        \
+  X(1, 16, 8, 3, 2, 1, 1, 4, 0, true)        \
+  X(2, 16, 8, 3, 2, 2, 1, 4, 0, true)        \
+  X(3, 16, 8, 2, 2, 2, 1, 4, 0, true)        \
+  X(4, 16, 4, 2, 2, 1, 1, 2, 0, true)        \
+  X(5, 16, 4, 3, 2, 2, 1, 2, 0, true)        \
+  X(6, 8, 16, 3, 2, 2, 1, 4, 0, true)        \
+  X(7, 16, 8, 1, 2, 1, 1, 4, 2, true)        \
+  X(8, 16, 4, 6, 2, 2, 1, 2, 0, true)        \
+  X(9, 16, 8, 3, 2, 3, 1, 4, 0, true)
 
 extern "C" int ring_lab(int v, int ex, int64_t n, const void *in, void *out, void *status, void *ticket,
                         uint32_t epoch, void *stream) {
@@ -442,8 +466,8 @@ extern "C" int ring_lab(int v, int ex, int64_t n, const void *in, void *out, voi
   uint64_t *stt = (uint64_t *)status;
   unsigned long long *tk = (unsigned long long *)ticket;
   switch (v) {
-#define C(id, W, R, S, F, NLB, CC, P, E) \
-  case id: return run<W, R, S, F, NLB, CC, P, E>(ex, n, i, o, stt, tk, epoch, s);
+#define C(id, W, R, S, F, NLB, CC, P, E, D) \
+  case id: return run<W, R, S, F, NLB, CC, P, E, D>(ex, n, i, o, stt, tk, epoch, s);
     V(C)
 #undef C
   }
@@ -451,7 +475,7 @@ extern "C" int ring_lab(int v, int ex, int64_t n, const void *in, void *out, voi
 }
 extern "C" int ring_lab_tile_elems(int v) {
   switch (v) {
-#define C(id, W, R, S, F, NLB, CC, P, E) \
+#define C(id, W, R, S, F, NLB, CC, P, E, D) \
   case id: return W * R * 128;
     V(C)
 #undef C
@@ -467,8 +491,8 @@ extern "C" int ring_lab_trace(int v, int64_t n, const void *in, void *out, void 
   uint64_t *stt = (uint64_t *)status;
   unsigned long long *tk = (unsigned long long *)ticket;
   switch (v) {
-#define C(id, W, R, S, F, NLB, CC, P, E) \
-  case id: return run<W, R, S, F, NLB, CC, P, E>(1, n, i, o, stt, tk, epoch, s, (uint64_t *)trace);
+#define C(id, W, R, S, F, NLB, CC, P, E, D) \
+  case id: return run<W, R, S, F, NLB, CC, P, E, D>(1, n, i, o, stt, tk, epoch, s, (uint64_t *)trace);
     V(C)
 #undef C
   }
