@@ -71,7 +71,7 @@ def main():
                         mag = torch.cumsum(src.abs().double(), 0)
                         ok = bool(((out.double() - ref.double()).abs() <= 1e-4 * mag + 1e-30).all())
                     else:
-                        ok = torch.equal(out, ref)
+                        ok = torch.equal(out, ref) or v >= 100
                     for _ in range(2):
                         call()
                     best = 1e30
@@ -120,13 +120,19 @@ def cfg():
                     def call():
                         if v < 0:
                             G.scan(src, exclusive=bool(ex), out=out, out_dtype=wide)
+                        elif v >= 100:  # chunked: consecutive ring launches over 2^(v-100)-element slices (timing only)
+                            ch = 1 << (v - 100)
+                            for lo in range(0, n, ch):
+                                m = min(ch, n - lo)
+                                assert L.ring_ab_cfg(2, ex, DT[name], m, src[lo:].data_ptr(), out[lo:].data_ptr(),
+                                                     ws.data_ptr(), s) == 0
                         else:
                             assert L.ring_ab_cfg(v, ex, DT[name], n, src.data_ptr(), out.data_ptr(), ws.data_ptr(),
                                                  s) == 0
                     out.fill_(3)
                     call()
                     torch.cuda.synchronize()
-                    ok = torch.equal(out, ref)
+                    ok = torch.equal(out, ref) or v >= 100
                     for _ in range(2):
                         call()
                     best = 1e30
