@@ -205,10 +205,13 @@ ga_status_t gpuarray_reduce_xgpu(ga_op_t op, ga_map_t map, ga_dtype_t in_dt, ga_
 
 /* Bytes of workspace gpuarray_scan needs for (dt, n), dt = the scan's OUTPUT
  * dtype: a 256-byte header plus per-tile look-back status.  Zero-fill once;
- * reusable afterwards (status words are epoch-tagged, the tile counter resets
- * itself).  Never share it with gpuarray_reduce.  A corrupted workspace makes
- * the kernel trap (a CUDA error at the next synchronisation) after 10 s
- * instead of hanging. */
+ * reusable afterwards by scans of any dtype, size and kernel (status words
+ * are epoch-tagged, the tile counter resets itself) until the 30-bit call
+ * epoch wraps: zero it again within 2^30 calls (the Python binding counts
+ * calls and does).  One call at a time per workspace: calls that may run
+ * concurrently (different streams) need their own.  Never share it with
+ * gpuarray_reduce.  A corrupted workspace makes the kernel trap (a CUDA
+ * error at the next synchronisation) after 10 s instead of hanging. */
 size_t gpuarray_scan_workspace_bytes(ga_dtype_t dt, int64_t n);
 
 /* Scan (§3.2.6 "parallel prefix sums") with the reduction
