@@ -150,9 +150,11 @@ ga_status_t gpuarray_elementwise(ga_ewop_t op, ga_dtype_t dt, int64_t n, const v
  * every device).  The workspace must be zero-filled ONCE when allocated; the
  * kernel leaves it reusable (block partials sit in slots tagged with a call
  * epoch that the finishing block advances; a slot is ready when it carries
- * the current call's tag — no reset, no atomics).  Calls
- * that may run concurrently need distinct workspaces, and a reduce workspace
- * must not be passed to gpuarray_scan (or vice versa): the layouts differ. */
+ * the current call's tag — no reset, no atomics) until the 31-bit tag
+ * wraps: zero it again within 2^31 calls (the Python binding counts calls
+ * and does).  Calls that may run concurrently need distinct workspaces, and
+ * a reduce workspace must not be passed to gpuarray_scan (or vice versa):
+ * the layouts differ. */
 size_t gpuarray_reduce_workspace_bytes(ga_dtype_t out_dt, int64_t n);
 
 /* *out = fold over i in [0, n) of map(x, y)[i] with `op`, starting from the
