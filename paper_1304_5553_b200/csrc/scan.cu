@@ -29,7 +29,7 @@
 // id resets the counter.
 // Tile 0's exclusive prefix is the carry-in c = sum(carry[0..carry_count)),
 // which is how a sharded scan injects the totals of earlier shards.
-// From 48 MiB of input up to 4 GiB (4-byte types), 768 MiB (8-byte) or
+// From 48 MiB of input up to 4 GiB (4-byte types), 2 GiB (8-byte) or
 // without bound (widening) the single-touch ring scan runs instead
 // (scan_ring.cuh: persistent CTAs, TMA stages, tiles held in registers while
 // they look back, 4-byte tiles prefetched into L2 one draw ahead): 3-19%
@@ -78,7 +78,7 @@ ga_status_t launch_scan(ga_op_t op, ga_scan_kind_t kind, ga_dtype_t in_dt, ga_dt
   const uintptr_t out_align = isz == osz ? 16 : 32;
   const bool aligned = ((uintptr_t)in & 15) == 0 && ((uintptr_t)out & (out_align - 1)) == 0;
   if (!aligned) return launch_shape<SHAPE_RG>(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);
-  if (use_ring(n, isz, osz)) return launch_ring(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);
+  if (use_ring(n, isz, osz, out)) return launch_ring(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);
   switch (choose_shape(n, isz, osz)) {
     case SHAPE_S: return launch_shape<SHAPE_S>(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);
     case SHAPE_M: return launch_shape<SHAPE_M>(op, ex, in_dt, dt, n, in, out, carry, carry_count, ws, s);

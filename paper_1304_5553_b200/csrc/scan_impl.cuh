@@ -169,18 +169,20 @@ constexpr int RING_W = 16, RING_R = 8, RING_S = 3, RING_F = 2;
 // input (int32 32 MiB: even; 64 MiB: -16%) up to
 //   4 GiB for 4-byte types (with the one-tile L2 prefetch: 2^28 -8%, 2^30
 //        -1 to -3%; 2^31: even to +6%, 2^32-2^33: even to +4%),
-//   768 MiB for 8-byte types (512 MiB: -3 to -5%; 1 GiB: even; beyond it
-//        +2 to +15%),
+//   2 GiB for 8-byte types (1 KiB rows and the prefetch: 2^27 -5 to -9%,
+//        2^28 -2 to -5%; 2^29-2^30: -4 to +6%), which needs a 32-byte
+//        aligned output (else the two-touch shapes run),
 //   any size for widening scans (4-byte in, 8-byte out: -17% at 64 MiB, -7%
 //        at 1 GiB, -5% at 4 GiB for SUM; the input arrives at a third of the
 //        traffic rate, so the on-chip buffer covers the look-back; MAX within
 //        +-1.4%).
-constexpr int64_t RING_MIN_BYTES = 48ll << 20, RING_MAX_BYTES4 = 4ll << 30, RING_MAX_BYTES8 = 768ll << 20;
-inline bool use_ring(int64_t n, size_t isz, size_t osz) {
+constexpr int64_t RING_MIN_BYTES = 48ll << 20, RING_MAX_BYTES4 = 4ll << 30, RING_MAX_BYTES8 = 2ll << 30;
+inline bool use_ring(int64_t n, size_t isz, size_t osz, const void *out) {
   const int64_t b = n * (int64_t)isz;
   if (b < RING_MIN_BYTES) return false;
   if (isz != osz) return true;
-  return b <= (isz == 8 ? RING_MAX_BYTES8 : RING_MAX_BYTES4);
+  if (isz == 8) return b <= RING_MAX_BYTES8 && ((uintptr_t)out & 31) == 0;
+  return b <= RING_MAX_BYTES4;
 }
 ga_status_t launch_ring(ga_op_t op, bool ex, ga_dtype_t in_dt, ga_dtype_t dt, int64_t n, const void *in, void *out,
                         const void *carry, int64_t cc, void *ws, cudaStream_t s);

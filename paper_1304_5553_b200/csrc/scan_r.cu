@@ -13,22 +13,29 @@ namespace {
 using namespace scan_detail;
 
 // Q: bulk loads in flight per CTA, PFN: tile ids drawn ahead and prefetched
-// into L2 (0 / -1 = the product choice).  4-byte scans: one bulk load in
-// flight (the next id is drawn once the previous load has landed, which
-// narrows the spread of landing times the look-back waits on) plus one id
-// drawn ahead whose input the producer prefetches into L2, so the HBM read
-// of the next tile overlaps and its bulk copy hits L2: int32 2^26 -10%,
-// 2^28 -8%, 2^30 -1 to -3% against the two-touch L shape.  8-byte and
-// widening scans: all S stages in flight, no prefetch (neither knob helped
-// them; tools/lab/run_ring_ab.py cfg, profiles/r2_ring.md).
-template <int OP, typename T, typename Tin, bool EX, int W = RING_W, int R = RING_R, int S = RING_S,
-          int F = RING_F, int Q0 = 0, int PFN0 = -1>
+// into L2, H: 16-byte chunks per lane per warp row (0 / -1 = the product
+// choice).  Non-widening scans: one bulk load in flight (the next id is
+// drawn once the previous load has landed, which narrows the spread of
+// landing times the look-back waits on) plus one id drawn ahead whose input
+// the producer prefetches into L2, so the HBM read of the next tile overlaps
+// and its bulk copy hits L2 — int32 2^26 -10%, 2^28 -8%, 2^30 -1 to -3%
+// against the two-touch L shape; 8-byte types also take 1 KiB rows (32
+// bytes per lane: half the 64-bit warp scans per element; the output must be
+// 32-byte aligned) — int64 -5 to -9% at 2^24-2^27 against the 512-byte-row
+// ring, and ahead of the L shape up to 2^28.  Widening scans: all S stages
+// in flight, no prefetch, 512-byte rows (neither knob helped them).
+// tools/lab/run_ring_ab.py cfg, profiles/r2_ring.md.
+template <int OP, typename T, typename Tin, bool EX, int W = RING_W, int R0 = 0, int S = RING_S, int F = RING_F,
+          int Q0 = 0, int PFN0 = -1, int H0 = 0>
 ga_status_t ring_run(int64_t n, const void *in, void *out, const void *carry, int64_t cc, void *ws, cudaStream_t s) {
-  constexpr int Q = Q0 > 0 ? Q0 : sizeof(T) == 4 ? 1 : S;
-  constexpr int PFN = PFN0 >= 0 ? PFN0 : sizeof(T) == 4 ? 1 : 0;
-  constexpr int64_t TE = (int64_t)W * R * 512 / (int64_t)sizeof(Tin);
-  constexpr size_t SMEM = (size_t)S * W * R * 512;
-  auto k = scan_ring_kernel<OP, T, Tin, W, R, S, F, EX, Q, PFN>;
+  constexpr bool WIDEN = sizeof(T) != sizeof(Tin);
+  constexpr int H = H0 > 0 ? H0 : (!WIDEN && sizeof(T) == 8) ? 2 : 1;
+  constexpr int R = R0 > 0 ? R0 : RING_R / H;  // 64 KiB tiles
+  constexpr int Q = Q0 > 0 ? Q0 : WIDEN ? S : 1;
+  constexpr int PFN = PFN0 >= 0 ? PFN0 : WIDEN ? 0 : 1;
+  constexpr int64_t TE = (int64_t)W * R * 512 * H / (int64_t)sizeof(Tin);
+  constexpr size_t SMEM = (size_t)S * W * R * 512 * H;
+  auto k = scan_ring_kernel<OP, T, Tin, W, R, S, F, EX, Q, PFN, H>;
   const cudaError_t attr = allow_dyn_smem((const void *)k, SMEM);
   if (attr != cudaSuccess) return fail(GA_ERR_CUDA, "scan (ring): %s", cudaGetErrorString(attr));
   ScanArgs<T, Tin> p = make_args<T, Tin>(n, TE, in, out, carry, cc, ws);

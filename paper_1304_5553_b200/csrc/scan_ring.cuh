@@ -75,14 +75,19 @@ constexpr int ring_threads() {
 // converted where it is folded; a row then stores 32 bytes per lane.
 // PFN: tile ids drawn this many uses ahead, their input prefetched into L2
 // (cp.async.bulk.prefetch.L2) so that the stage's bulk copy later hits L2.
-template <int OP, typename T, typename Tin, int W, int R, int S, int F, bool EXCLUSIVE, int MAXQ = S, int PFN = 0>
+// H: 16-byte chunks per lane per warp row (1: 512-byte rows; 2: 1 KiB rows,
+// 32 bytes per lane — half the warp scans per element, 32-byte stores).
+template <int OP, typename T, typename Tin, int W, int R, int S, int F, bool EXCLUSIVE, int MAXQ = S, int PFN = 0,
+          int H = 1>
 __global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(ScanArgs<T, Tin> p) {
   pdl_enter();
   using O = Op<OP, T>;
   using namespace ring;
-  constexpr int E = 16 / (int)sizeof(Tin);  // elements per lane per 512-byte input row
-  constexpr int ROW = 32 * E;
-  constexpr int TB = W * R * 512;  // tile input bytes
+  constexpr int E = 16 / (int)sizeof(Tin);  // elements per 16-byte chunk
+  constexpr int EL = E * H;                  // elements per lane per warp row
+  constexpr int RB = 512 * H;                // input bytes per warp row
+  constexpr int ROW = 32 * EL;
+  constexpr int TB = W * R * RB;  // tile input bytes
   constexpr int64_t TE = TB / (int64_t)sizeof(Tin);
   constexpr bool WIDEN = sizeof(T) != sizeof(Tin);
   static_assert(!WIDEN || (sizeof(T) == 8 && sizeof(Tin) == 4), "widening is 4 -> 8 bytes");
@@ -301,76 +306,93 @@ __global__ void __launch_bounds__(ring_threads<W, F>(), 1) scan_ring_kernel(Scan
   if (warp < W) {  // -------------------------------------------------------------- data
     // load(k): wait for use k's stage, copy this warp's R rows into registers,
     // release the stage, fold the rows into wt; false at the sentinel.
-    auto load = [&](int64_t k, uint4 (&v)[R], int64_t &t) -> bool {
+    auto load = [&](int64_t k, uint4 (&v)[R][H], int64_t &t) -> bool {
       const int s = (int)(k % S);
       mb_wait(&full[s], (uint32_t)((k / S) & 1));
       t = *reinterpret_cast<volatile int64_t *>(&tid_ring[k % TR]);
       if (t >= nt) return false;
       const unsigned char *stage = smem + s * TB;
       const int64_t bulk = bulk_bytes(t);
-      const int off0 = warp * R * 512 + lane * 16;
+      const int off0 = warp * R * RB + lane * 16 * H;
       if (bulk == TB) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = *reinterpret_cast<const uint4 *>(stage + off0 + r * 512);
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int h = 0; h < H; ++h) v[r][h] = *reinterpret_cast<const uint4 *>(stage + off0 + r * RB + h * 16);
       } else {
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = chunk(stage, t, off0 + r * 512, bulk);
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int h = 0; h < H; ++h) v[r][h] = chunk(stage, t, off0 + r * RB + h * 16, bulk);
       }
       __syncwarp();
       if (lane == 0) mb_arrive(&empty[s]);
       T a = neutral;
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        T e[E];
-        unpack(v[r], e);
+      for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int q = 0; q < E; ++q) a = O::fold(a, e[q]);
-      }
+        for (int h = 0; h < H; ++h) {
+          T e[E];
+          unpack(v[r][h], e);
+#pragma unroll
+          for (int q = 0; q < E; ++q) a = O::fold(a, e[q]);
+        }
       a = warp_fold<OP, T>(a);
       if (lane == 0) wt[k % 3][warp] = a;
       asm volatile("bar.sync 3, %0;" ::"n"(W * 32) : "memory");
       return true;
     };
     // scan(k): wait for use k's prefix, scan the rows in order, store.
-    auto scan = [&](int64_t k, const uint4 (&v)[R], int64_t t) {
+    auto scan = [&](int64_t k, const uint4 (&v)[R][H], int64_t t) {
       const uint64_t drop = l2::policy_evict_first();
       mb_wait(&pref[k % TR], (uint32_t)((k / TR) & 1));
       T carry = pre_ring[k % TR];
       for (int i = 0; i < warp; ++i) carry = O::fold(carry, wt[k % 3][i]);
-      const int64_t i0 = t * TE + (int64_t)warp * R * ROW + lane * E;
+      const int64_t i0 = t * TE + (int64_t)warp * R * ROW + lane * EL;
       const bool full_tile = (t + 1) * TE <= p.n;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        T e[E], o[E];
-        unpack(v[r], e);
+        T e[EL], o[EL];
 #pragma unroll
-        for (int q = 1; q < E; ++q) e[q] = O::fold(e[q - 1], e[q]);
-        const T x = warp_inclusive<OP, T>(e[E - 1], lane);
+        for (int h = 0; h < H; ++h) {
+          T c[E];
+          unpack(v[r][h], c);
+#pragma unroll
+          for (int q = 0; q < E; ++q) e[h * E + q] = c[q];
+        }
+#pragma unroll
+        for (int q = 1; q < EL; ++q) e[q] = O::fold(e[q - 1], e[q]);
+        const T x = warp_inclusive<OP, T>(e[EL - 1], lane);
         const T cb = O::fold(carry, warp_exclusive_of<OP, T>(x, lane));
         carry = O::fold(carry, __shfl_sync(0xffffffffu, x, 31));
 #pragma unroll
-        for (int q = 0; q < E; ++q) {
+        for (int q = 0; q < EL; ++q) {
           if constexpr (EXCLUSIVE) o[q] = q == 0 ? cb : O::fold(cb, e[q - 1]);
           else o[q] = O::fold(cb, e[q]);
         }
         const int64_t i = i0 + (int64_t)r * ROW;
-        if (full_tile || i + E <= p.n) {
-          if constexpr (WIDEN) {  // 4 outputs of 8 bytes: one 32-byte store per lane
-            V32 w;
-#pragma unroll
-            for (int q = 0; q < E; ++q) vset<T>(w, q, o[q]);
-            l2::stg256v_hint(p.out + i, w, drop);
-          } else {
+        if (full_tile || i + EL <= p.n) {
+          constexpr int OB = EL * (int)sizeof(T);  // output bytes per lane: 16, 32 or 64
+          if constexpr (OB == 16) {
             l2::stg128_hint(p.out + i, Chunk<T>::pack(o), drop);
+          } else {  // 32-byte stores (the caller guarantees a 32-byte aligned output)
+            constexpr int EPV = 32 / (int)sizeof(T);
+#pragma unroll
+            for (int g = 0; g < OB / 32; ++g) {
+              V32 w;
+#pragma unroll
+              for (int q = 0; q < EPV; ++q) vset<T>(w, q, o[g * EPV + q]);
+              l2::stg256v_hint(p.out + i + g * EPV, w, drop);
+            }
           }
         } else {
 #pragma unroll
-          for (int q = 0; q < E; ++q)
+          for (int q = 0; q < EL; ++q)
             if (i + q < p.n) p.out[i + q] = o[q];
         }
       }
     };
-    uint4 va[R], vb[R];
+    uint4 va[R][H], vb[R][H];
     int64_t ta, tb;
     if (!load(0, va, ta)) return;
     for (int64_t k = 0;; k += 2) {

@@ -672,19 +672,23 @@ def test_ewmap_maxmin_signed_zero_bit_exact(dt):
         assert np.array_equal(bits(got[keep]), bits(ref[keep])), ew
 
 
-# 8-byte scans reach the L shape above the ring window (768 MiB of input)
+# 8-byte scans reach the L shape above the ring window (2 GiB of input) or,
+# from 96 MiB, when the output is 16- but not 32-byte aligned (the ring's
+# 1 KiB rows store 32 bytes per lane)
 N_L8 = (768 << 20) // 8 + 12345
+N_L8A = (2 << 30) // 8 + 12345
 
 
 @pytest.mark.parametrize("dt", [np.int64, np.float64])
 @pytest.mark.parametrize("offset", [0, 2])
 def test_scan_8byte_l_shape_both_row_widths(dt, offset):
     """8-byte scans at the L shape take 1 KiB rows (LDG/STG.256) when input and
-    output are 32-byte aligned, else 512-byte rows: a view 2 elements (16
-    bytes) into an allocation exercises the second path.  Integer scans are
-    exact; float64 SUM over integer-valued data (prefix sums < 2^53) is exact
-    in any order and must equal the integer oracle bit for bit."""
-    n = N_L8  # ragged last tile
+    output are 32-byte aligned (past 2 GiB here), else 512-byte rows: a view
+    2 elements (16 bytes) into an allocation exercises the second path.
+    Integer scans are exact; float64 SUM over integer-valued data (prefix
+    sums < 2^53) is exact in any order and must equal the integer oracle bit
+    for bit."""
+    n = N_L8A if offset == 0 else N_L8  # ragged last tile
     if dt == np.int64:
         x = np.random.default_rng(offset + 5).integers(-(1 << 40), 1 << 40, size=n, dtype=np.int64)
     else:
@@ -700,11 +704,12 @@ def test_scan_8byte_l_shape_both_row_widths(dt, offset):
 
 
 @pytest.mark.parametrize("offset", [0, 2])
-@pytest.mark.parametrize("n", [300 * 24 * 32 * 64 + 4097, N_L8])
+@pytest.mark.parametrize("n", [300 * 24 * 32 * 64 + 4097, N_L8A])
 def test_scan_int64_l_shape_in_place(offset, n):
-    """In-place int64 scans in the ring window (118 MB) and at the L shape,
-    1 KiB rows (offset 0) and 512-byte rows (offset 2 elements = 16 bytes):
-    coherent loads (the output overwrites the input) on every path."""
+    """In-place int64 scans: 118 MB (offset 0: the ring kernel; offset 2
+    elements = 16 bytes: the L shape with 512-byte rows) and past 2 GiB (the
+    L shape, 1 KiB rows at offset 0): coherent loads (the output overwrites
+    the input) on every path."""
     x = np.random.default_rng(77 + offset).integers(-(1 << 40), 1 << 40, size=n, dtype=np.int64)
     for exclusive in (False, True):
         d = to_dev(x, offset)
@@ -718,7 +723,7 @@ def test_scan_int64_l_shape_in_place(offset, n):
 def test_scan_maxmin_8byte_l_shape(dt, op):
     """MAX / MIN scans of 8-byte types at the L shape (1 KiB rows), inclusive
     and exclusive, bit-exact — float64 data zero- and NaN-heavy (R6, R7)."""
-    n = N_L8 - 12345 + 999
+    n = N_L8A - 12345 + 999  # past the ring window: the L shape, 1 KiB rows
     if dt == np.int64:
         x = np.random.default_rng(op + 3).integers(-(1 << 62), 1 << 62, size=n, dtype=np.int64)
     else:
@@ -731,15 +736,16 @@ def test_scan_maxmin_8byte_l_shape(dt, op):
 
 
 # ------------------------------------------------------------------ ring scan (scan_ring.cuh)
-# 16-byte aligned scans of 48 MiB .. 4 GiB (4-byte) / 768 MiB (8-byte) of
-# input, and widening scans from 48 MiB, take the single-touch ring kernel:
-# 64 KiB tiles (16384 / 8192 elements), persistent CTAs, TMA stages, 4-byte
-# tiles prefetched into L2 one draw ahead, a ragged tail read element by
-# element past the last 16-byte multiple.  (The 4-byte upper edge, n = 2^30,
+# 16-byte aligned scans of 48 MiB .. 4 GiB (4-byte) / 2 GiB (8-byte, with a
+# 32-byte aligned output) of input, and widening scans from 48 MiB, take the
+# single-touch ring kernel: 64 KiB tiles (16384 / 8192 elements), persistent
+# CTAs, TMA stages, non-widening tiles prefetched into L2 one draw ahead,
+# 1 KiB rows for 8-byte types, a ragged tail read element by element past
+# the last 16-byte multiple.  (The 4-byte upper edge, n = 2^30,
 # is C3's size: test_parity_full_gpu compares that scan whole; the L shape
 # beyond it is C5's 2^33 scan, also compared whole.)
 RING_MIN = 48 << 20
-RING_MAX = {4: 4 << 30, 8: 768 << 20}
+RING_MAX = {4: 4 << 30, 8: 2 << 30}
 
 
 def _ring_data(dt, op, n, seed):
@@ -800,7 +806,7 @@ def test_scan_ring_window_edges(dt):
     info = np.iinfo(dt)
     for n in (lo - 1, lo, lo + 1, 1000 * te + 3) + ((hi, hi + 1) if isz == 8 else ()):
         x = np.random.default_rng(n).integers(info.min, info.max, size=n, dtype=dt, endpoint=True)
-        for exclusive in (False, True):
+        for exclusive in ((False, True) if n < hi else (False,)):
             kind = oracle.EXCLUSIVE if exclusive else oracle.INCLUSIVE
             got = G.scan(to_dev(x), exclusive=exclusive).cpu().numpy()
             assert_bit_exact(got, oracle.scan(kind, x))
@@ -809,8 +815,10 @@ def test_scan_ring_window_edges(dt):
 @pytest.mark.parametrize("dt", [np.int32, np.int64, np.float32])
 def test_scan_ring_carry_inplace_and_views(dt):
     """Ring-window sizes with a carry-in (tile 0 publishes carry (+) aggregate),
-    in place, and as a view 16 bytes into its allocation (still the ring
-    kernel) or 1 element in (the unaligned register kernel)."""
+    in place, and as a view 16 bytes into its allocation (4-byte: still the
+    ring kernel; 8-byte: the two-touch M/L shapes, the ring's 1 KiB rows
+    needing a 32-byte aligned output) or 1 element in (the unaligned
+    register kernel)."""
     isz = np.dtype(dt).itemsize
     n = (96 << 20) // isz + 5
     if np.dtype(dt).kind == "f":

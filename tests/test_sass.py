@@ -77,9 +77,10 @@ def test_vector_widths(sass):
                 st = r"STG\.E\S*\.256" if widen else r"STG\.E\S*\.128"  # widened rows: 32 B per lane
                 assert re.search(r"LDG\.E\S*\.128", body) and re.search(st, body), d
             seen["scan"] = True
-        if "scan_ring_kernel" in d:  # TMA bulk copies in (UBLKCP); rows out: 16 B per lane (32 B widened)
-            widen = "ScanArgs<double, float>" in d or "ScanArgs<long, int>" in d
-            st = r"STG\.E\S*\.256" if widen else r"STG\.E\S*\.128"
+        if "scan_ring_kernel" in d:  # TMA bulk copies in (UBLKCP); data rows out (.NA, streaming): 16 B per
+            # lane for 4-byte scans, 32 B for 8-byte (1 KiB rows) and widened ones
+            four = "ScanArgs<int, int>" in d or "ScanArgs<float, float>" in d
+            st = r"STG\.E\.NA\S*\.128" if four else r"STG\.E\.NA\S*\.256"
             assert "UBLKCP" in body and re.search(st, body), d
             seen["ring"] = True
     assert all(seen.values()), seen

@@ -31,11 +31,11 @@ DEV = "cuda:0"
 # S / M / L super-tile shapes for 4-byte and 8-byte scans (scan_impl.cuh
 # choose_shape: L from 256 tiles of 98304 (4-byte) / 49152 (8-byte) elements,
 # M from 64 tiles of 32768 / 16384) and the ring kernel, which takes scans of
-# 48 MiB .. 4 GiB (4-byte) / 768 MiB (8-byte) of input and widening scans
+# 48 MiB .. 4 GiB (4-byte) / 2 GiB (8-byte) of input and widening scans
 # from 48 MiB (its own ticket-reset rule: every CTA draws one id past the last
 # tile).  "R" runs the ring for every scan here; "L" runs the L shape for the
 # int64 scans, between ring-kernel int32 and widening scans.
-SIZES = {"S": 100_003, "M": 3_000_017, "R": 26_000_003, "L": (768 << 20) // 8 + 4099}
+SIZES = {"S": 100_003, "M": 3_000_017, "R": 26_000_003, "L": (2 << 30) // 8 + 4099}
 TDT = {np.int32: torch.int32, np.int64: torch.int64, np.float32: torch.float32, np.float64: torch.float64}
 GADT = {np.int32: 2, np.int64: 3, np.float32: 0, np.float64: 1}
 

@@ -46,21 +46,17 @@ extern "C" int ring_ab(int op, int ex, int dt, int64_t n, const void *in, void *
 template <typename T, typename Tin = T>
 static int ring_cfg(int v, int ex, int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   using namespace ga::scan_impl;
-#define RC(W, R, S, F, Q, PF)                                                                                   \
-  return (int)(ex ? ring_run<GA_OP_SUM, T, Tin, true, W, R, S, F, Q, PF>(n, in, out, nullptr, 0, ws, s)        \
-                  : ring_run<GA_OP_SUM, T, Tin, false, W, R, S, F, Q, PF>(n, in, out, nullptr, 0, ws, s));
+#define RC(W, R, S, F, Q, PF, H)                                                                                \
+  return (int)(ex ? ring_run<GA_OP_SUM, T, Tin, true, W, R, S, F, Q, PF, H>(n, in, out, nullptr, 0, ws, s)     \
+                  : ring_run<GA_OP_SUM, T, Tin, false, W, R, S, F, Q, PF, H>(n, in, out, nullptr, 0, ws, s));
   switch (v) {
-    case 1: RC(16, 8, 3, 2, 0, 0)
-    case 2: RC(16, 8, 3, 2, 0, 1)
-    case 3: RC(16, 8, 3, 2, 1, 1)
-    case 4: RC(16, 8, 3, 2, 1, 2)
-    case 5: RC(16, 8, 3, 2, 2, 1)
-    case 6: RC(16, 8, 3, 2, 1, 0)
-    case 7: RC(16, 8, 3, 2, 2, 2)
-    case 8: RC(16, 8, 3, 2, 3, 0)
-    case 9: RC(16, 8, 3, 2, 3, 1)
-    case 10: RC(16, 8, 3, 2, 3, 3)
-    case 11: RC(16, 8, 3, 2, 2, 3)
+    case 1: RC(16, 8, 3, 2, 0, -1, 1)
+    case 2: RC(16, 4, 3, 2, 0, -1, 2)
+    case 3: RC(16, 4, 3, 2, 1, 1, 2)
+    case 4: RC(16, 4, 3, 2, 3, 0, 2)
+    case 5: RC(16, 4, 3, 2, 1, 0, 2)
+    case 6: RC(16, 4, 3, 2, 2, 1, 2)
+    case 7: RC(16, 0, 3, 2, 0, -1, 0)
   }
 #undef RC
   return 2;

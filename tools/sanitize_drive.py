@@ -95,8 +95,8 @@ for n, dt in (((48 << 20) // 4 + 3, torch.int32), ((64 << 20) // 8 + 1, torch.in
 # plus a ragged tail (8-byte and widened L-shape scans read 1 KiB rows when
 # 32-byte aligned and 512-byte rows otherwise: both, via a 2-element
 # (16-byte) view offset)
-for n, dt in (((384 << 20) // 4 + 12345, torch.int32), ((768 << 20) // 8 + 777, torch.int64),
-              ((768 << 20) // 8 + 999, torch.float64)):
+for n, dt in (((4 << 30) // 4 + 12345, torch.int32), ((2 << 30) // 8 + 777, torch.int64),
+              ((2 << 30) // 8 + 999, torch.float64)):
     for off in (0, 2):
         x = arr(n, dt, off)
         G.scan(x)
