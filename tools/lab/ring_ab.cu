@@ -50,13 +50,11 @@ static int ring_cfg(int v, int ex, int64_t n, const void *in, void *out, void *w
   return (int)(ex ? ring_run<GA_OP_SUM, T, Tin, true, W, R, S, F, Q, PF, H>(n, in, out, nullptr, 0, ws, s)     \
                   : ring_run<GA_OP_SUM, T, Tin, false, W, R, S, F, Q, PF, H>(n, in, out, nullptr, 0, ws, s));
   switch (v) {
-    case 1: RC(16, 8, 3, 2, 0, -1, 1)
-    case 2: RC(16, 4, 3, 2, 0, -1, 2)
-    case 3: RC(16, 4, 3, 2, 1, 1, 2)
-    case 4: RC(16, 4, 3, 2, 3, 0, 2)
-    case 5: RC(16, 4, 3, 2, 1, 0, 2)
-    case 6: RC(16, 4, 3, 2, 2, 1, 2)
-    case 7: RC(16, 0, 3, 2, 0, -1, 0)
+    case 1: RC(16, 0, 3, 2, 0, -1, 0)
+    case 2: RC(16, 4, 3, 2, 0, -1, 1)
+    case 3: RC(16, 2, 3, 2, 0, -1, 1)
+    case 4: RC(16, 4, 3, 2, 3, 0, 1)
+    case 5: RC(16, 2, 3, 2, 3, 0, 1)
   }
 #undef RC
   return 2;
