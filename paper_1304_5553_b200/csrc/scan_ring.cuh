@@ -1,13 +1,15 @@
-// scan_ring.cuh — the single-touch "ring" scan for mid-size arrays
-// (§3.2.6; scan expressions of P:479-485), used by scan.cu
-// for 16-byte aligned, non-widening scans whose input spans
-// RING_MIN_BYTES .. RING_MAX_BYTES (profiles/r2_scan.md, third pass).
+// scan_ring.cuh — the single-touch "ring" scan (§3.2.6;
+// scan expressions of P:479-485), used by scan.cu for 16-byte aligned scans
+// of 48 MiB .. 4 GiB (4-byte) / 2 GiB (8-byte) of input and for widening
+// scans from 48 MiB (scan_impl.cuh use_ring; profiles/r2_ring.md).
 //
 // Persistent CTAs, one per SM, draw 64 KiB tiles from the workspace ticket
 // (the same {epoch | counter} word, status layout and look-back as the
 // two-touch kernel), so every HBM byte is read once and written once:
 //   warp W       producer: draws tile ids and fills a ring of S shared-memory
-//                stages with TMA bulk copies (cp.async.bulk, mbarrier);
+//                stages with TMA bulk copies (cp.async.bulk, mbarrier); for
+//                non-widening scans it keeps one copy in flight and draws one
+//                id ahead whose input it prefetches into L2;
 //   warps W+2..  fold: fold each stage as it lands and publish the tile's
 //                AGGREGATE at once (tile 0: its INCLUSIVE value with the
 //                carry-in), so no aggregate waits behind a look-back;
@@ -15,16 +17,18 @@
 //                each tile in turn, publishes INCLUSIVE, hands the prefix on;
 //   warps 0..W-1 data: copy a landed stage into registers and release it at
 //                once, fold their rows, wait for the tile's prefix, scan the
-//                rows and store them (512 B per warp instruction).  They hold
-//                TWO tiles: tile k waits for its prefix while tile k+1 is
-//                already out of its stage, so the stages keep streaming.
+//                rows and store them (512-byte rows; 1 KiB for 8-byte types).
+//                They hold TWO tiles: tile k waits for its prefix while tile
+//                k+1 is already out of its stage, so the stages keep
+//                streaming.
 // Per-use values (tile id, aggregate, prefix and their mbarriers) live in
 // rings of TR slots, so a role running ahead never overwrites what a slower
-// one still needs.  Against the two-touch kernel (same process, back to back):
-// int32 2^24 -12%, 2^25 -12%, 2^26 -8 to -10%, 2^27 even, 2^28 +5%; beyond
-// that a tile's prefix arrives ~10 us after it lands (it needs every earlier
-// tile's aggregate), more than the 320 KiB per SM of stages and registers
-// can cover, and the L2-buffered two-touch kernel wins.
+// one still needs.  Against the two-touch kernel: int32 2^26 -10%, 2^28 -8%
+// (336-343 us, 91% of the 1:1 copy), 2^30 -1 to -3%; int64 2^27 -5 to -9%.
+// Beyond the window the L2-buffered two-touch kernel is as fast or faster:
+// a tile's prefix arrives ~8-10 us after it lands (it needs every earlier
+// tile's aggregate), and the per-SM buffer of stages, registers and one
+// prefetched tile only covers that up to a few GiB.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
