@@ -40,9 +40,11 @@ def main():
     sink = torch.empty((), dtype=torch.float32, device=dev)
     N = 1 << hi
     k32 = synth.device_fill(synth.I32_RANGE, 3, N, lo=0, hi=9, device=dev)
-    k64 = synth.device_fill(synth.I64_RANGE, 3, N, lo=0, hi=9, device=dev)
-    o32, o64 = torch.empty_like(k32), torch.empty_like(k64)
-    ws = torch.zeros(256 + 32 * N // 64 + (1 << 20), dtype=torch.uint8, device=dev)
+    need64 = any(L.lab_scan_elem_bytes(v) == 8 for v in variants)
+    k64 = synth.device_fill(synth.I64_RANGE, 3, N, lo=0, hi=9, device=dev) if need64 else None
+    o32 = torch.empty_like(k32)
+    o64 = torch.empty_like(k64) if need64 else None
+    ws = torch.zeros(256 + 32 * (N // 4096) + (1 << 20), dtype=torch.uint8, device=dev)
     s = torch.cuda.current_stream().cuda_stream
     for lg in range(lo, hi + 1):
         n = 1 << lg

@@ -58,7 +58,11 @@ static int run(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   X(47, int32_t, 24, 32, 32, 42, 16, 8, 16)       \
   X(46, int64_t, 24, 32, 32, 42, 4, 4, 8)         \
   X(50, int64_t, 24, 32, 32, 42, 4, 4, 16)        \
-  X(51, int64_t, 24, 32, 32, 42, 4, 8, 8)
+  X(51, int64_t, 24, 32, 32, 42, 4, 8, 8)         \
+  X(170, int32_t, 24, 32, 32, 21, 8, 8, 8)         \
+  X(171, int32_t, 24, 32, 32, 84, 8, 8, 8)         \
+  X(172, int32_t, 24, 32, 32, 148, 8, 8, 8)        \
+  X(173, int32_t, 24, 32, 32, 296, 8, 8, 8)
 
 // 1 KiB rows (RB = 1024: LDG/STG.256): T, warps, rows, UNROLL, P1U, PF rows, distance
 template <typename T, int W, int R, int U, int P1, int PF, int DIST, bool EX = true>
