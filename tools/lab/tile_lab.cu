@@ -62,7 +62,11 @@ static int run(int64_t n, const void *in, void *out, void *ws, cudaStream_t s) {
   X(170, int32_t, 24, 32, 32, 21, 8, 8, 8)         \
   X(171, int32_t, 24, 32, 32, 84, 8, 8, 8)         \
   X(172, int32_t, 24, 32, 32, 148, 8, 8, 8)        \
-  X(173, int32_t, 24, 32, 32, 296, 8, 8, 8)
+  X(173, int32_t, 24, 32, 32, 296, 8, 8, 8)       \
+  X(174, int32_t, 24, 32, 32, 32, 8, 8, 8)        \
+  X(175, int32_t, 24, 32, 32, 37, 8, 8, 8)        \
+  X(176, int32_t, 24, 32, 32, 48, 8, 8, 8)        \
+  X(177, int32_t, 24, 32, 32, 56, 8, 8, 8)
 
 // 1 KiB rows (RB = 1024: LDG/STG.256): T, warps, rows, UNROLL, P1U, PF rows, distance
 template <typename T, int W, int R, int U, int P1, int PF, int DIST, bool EX = true>
