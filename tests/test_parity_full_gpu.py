@@ -123,6 +123,19 @@ def test_c3_int_sum_max_scan_2p30(dt):
     _check_scan_full(out, n, kind, 3, 0, 9, npdt, exclusive=False)
 
 
+@pytest.mark.parametrize("n,exclusive", [((1 << 30), True), ((1 << 30) + 5, False)])
+def test_int32_scan_at_the_ring_windows_upper_edge(n, exclusive):
+    """4 GiB of int32 input is the last size the ring kernel takes (with its
+    one-tile L2 prefetch); 5 elements more go to the two-touch L shape.  Both
+    sides of the edge, every element against the chunked oracle."""
+    need_bytes(2 * n * 4)
+    k = synth.device_fill(synth.I32_RANGE, 3, n, lo=0, hi=9, device=DEV)
+    out = G.scan(k, exclusive=exclusive)
+    del k
+    free()
+    _check_scan_full(out, n, synth.I32_RANGE, 3, 0, 9, np.int32, exclusive=exclusive)
+
+
 def _check_scan_full(out, n, kind, seed, lo, hi, npdt, exclusive):
     """Every element of the device scan output against the chunked oracle."""
     def fetch(start, m, dest):
